@@ -1,0 +1,146 @@
+/*
+ * gapsafe_b200 -- C ABI of the B200-native Gap Safe Lasso hot path.
+ *
+ * This is the drop-in boundary.  The reference package
+ * (/root/reference/pkg/src/gapsafe) has no FFI layer of its own; its
+ * "operator API" for the path is (1) the in-place numba kernels of
+ * _kernels.py, (2) the DesignMatrix method set and (3) the public solver
+ * entry points.  Each entry point below names the reference interface it
+ * replaces.  Plain pointers and sizes only: every host pointer is borrowed for
+ * the duration of the call; device buffers are owned by the handles.
+ *
+ * Errors: functions return GS_OK (0) or a negative code; gs_last_error()
+ * gives a thread-local message.  The codes map onto the reference's Python
+ * exceptions (problem.py:12, regions.py:19, solver.py:86-87,
+ * design_matrix.py:96-98).  There is no CPU fallback: without a CUDA device
+ * every call fails with GS_ERR_NODEVICE.
+ */
+#ifndef GAPSAFE_B200_H
+#define GAPSAFE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_OK 0
+#define GS_ERR_CUDA (-1)        /* CUDA runtime failure                        */
+#define GS_ERR_VALUE (-2)       /* ValueError                                  */
+#define GS_ERR_INDEX (-3)       /* IndexError (design_matrix.py:96-98)         */
+#define GS_ERR_RUNTIME (-4)     /* RuntimeError: zero-norm active column       */
+#define GS_ERR_INFEASIBLE (-5)  /* InfeasibleDualError (problem.py:12,74-76)   */
+#define GS_ERR_NUMERICAL (-6)   /* NumericalInconsistencyError (regions.py:19) */
+#define GS_ERR_NODEVICE (-7)    /* no CUDA device: fail loudly, never fall back */
+
+#define GS_DTYPE_F64 0
+#define GS_DTYPE_F32 1
+
+#define GS_RULE_NONE 0          /* solver.py:27 Rule.NONE       */
+#define GS_RULE_GAP_SPHERE 1    /* solver.py:31 Rule.GAP_SPHERE */
+
+typedef struct gs_matrix gs_matrix;
+typedef struct gs_solver gs_solver;
+
+/* ---- runtime ------------------------------------------------------------ */
+int gs_init(int device);
+int gs_device_count(int *count);
+const char *gs_last_error(void);
+const char *gs_version(void);
+
+/* ---- DesignMatrix storage (design_matrix.py:34-57) ----------------------- */
+/* Dense column-major design, column j at X + j*ld_host (F-order numpy array).
+ * dtype GS_DTYPE_F64 or GS_DTYPE_F32 (fp32 storage, fp64 arithmetic).
+ * norms_sq: optional host column norms^2 (else computed on the device). */
+int gs_matrix_dense(const void *X, int dtype, int64_t n, int64_t p, int64_t ld_host,
+                    const double *norms_sq, gs_matrix **out);
+/* Canonical CSC (sorted, deduplicated), design_matrix.py:37-43. */
+int gs_matrix_csc(const double *data, const int32_t *indices, const int64_t *indptr,
+                  int64_t n, int64_t p, const double *norms_sq, gs_matrix **out);
+int gs_matrix_norms_sq(const gs_matrix *M, double *out);              /* col_norms_sq */
+int64_t gs_matrix_device_bytes(const gs_matrix *M);
+void gs_matrix_free(gs_matrix *M);
+
+/* ---- DesignMatrix primitives ---------------------------------------------- */
+/* X^T v (cols == NULL: all p columns, design_matrix.py:144-149) or restricted
+ * to cols (_kernels.py:14-36 tdot_dense/tdot_csc).  exact_order = 1 uses the
+ * reference's sequential non-FMA order (bit-exact with _kernels.py). */
+int gs_tdot(const gs_matrix *M, const double *v, const int64_t *cols, int64_t k,
+            double tail_scale, double *out, int exact_order);
+/* X @ beta (design_matrix.py:130-137). */
+int gs_matvec(const gs_matrix *M, const double *beta, double *out);
+/* (max_j |x_j^T v|, argmax), smallest index on ties (design_matrix.py:160-174). */
+int gs_max_abs_correlation(const gs_matrix *M, const double *v, const int64_t *restrict_cols,
+                           int64_t k, double *val, int64_t *arg);
+/* v += a * x_j (design_matrix.py:115-128). */
+int gs_axpy_col(const gs_matrix *M, int64_t j, double a, double *v);
+
+/* ---- kernel twin of the CD epoch (_kernels.py:39-92, solver.py:82-101) --- */
+/* beta, rho updated in place.  norms_sq NULL: the matrix's own.  exact_order = 1
+ * reproduces the reference arithmetic bit for bit; 0 runs the production
+ * kernel (CTA-parallel dot, certified-zero skipping). */
+int gs_cd_pass(const gs_matrix *M, double *beta, double *rho, const int64_t *active, int64_t k,
+               double lam, const double *norms_sq, double tail_scale, int exact_order);
+
+/* ---- sphere screening (regions.py:75-79,129-139) --------------------------- */
+/* mu_j = |x_j^T center| + radius*||x_j||, active = {mu >= 1 - tol} ascending.
+ * cols NULL: all p.  mu (len k or p) may be NULL. */
+int gs_screen_sphere(const gs_matrix *M, const double *center, double radius, const int64_t *cols,
+                     int64_t k, double tol, double *mu, int64_t *active_out, int64_t *n_active);
+
+/* device reductions for the problem.py scalar algebra: dot = a.b (b may be
+ * NULL), asum = sum |a|. */
+int gs_vec_stats(const double *a, const double *b, int64_t n, double *dot, double *asum);
+
+/* ---- solver (solver.py:149-246) and path driver support (path.py:52-105) - */
+typedef void (*gs_ckpt_cb)(const int64_t *active, int64_t n_active, void *user);
+
+typedef struct {
+    double epsilon;          /* absolute gap tolerance (solver.py:37)   */
+    int64_t max_passes;      /* solver.py:38                            */
+    int64_t screen_every;    /* solver.py:39                            */
+    int32_t rule;            /* GS_RULE_*                               */
+    int32_t certify;         /* 1: certified-zero skipping in CD (exact) */
+    gs_ckpt_cb on_checkpoint;/* solver.py:41-45 hook (NULL: none)      */
+    void *user;
+} gs_solve_config;
+
+typedef struct {
+    /* caller-provided host buffers (NULL: not copied) */
+    double *beta;            /* [p] */
+    double *residual;        /* [n] */
+    double *theta;           /* [n] */
+    int64_t *active;         /* [p] */
+    int64_t *trace_passes;   /* [trace_cap] */
+    int64_t *trace_active;
+    double *trace_gap;
+    double *trace_radius;
+    int64_t trace_cap;
+    /* outputs */
+    int64_t n_active, n_trace, passes_done;
+    int32_t converged, interpolating, lambda_max_shortcut, pad_;
+    double margin, primal, dual, gap;
+    uint64_t cd_visits, cd_uncertified, cd_nonzero;
+    int64_t checkpoints;
+    double device_ms;
+} gs_solve_result;
+
+/* y is uploaded once; lambda_max = |X^T y|_inf is computed once and cached
+ * (problem.py:50 recomputes it per LassoProblem; the value is identical). */
+int gs_solver_create(const gs_matrix *M, const double *y, gs_solver **out);
+int gs_solver_lambda_max(gs_solver *S, double *lambda_max, int64_t *j_star, double *y_norm_sq);
+/* warm start (solver.py:164-169): beta == NULL -> zeros */
+int gs_solver_set_beta(gs_solver *S, const double *beta);
+/* Sequential gap-sphere screen at lam from the previous solve's (beta, theta,
+ * residual) (path.py:82-91): leaves active0 on the device for the next solve. */
+int gs_solver_seq_screen(gs_solver *S, double lam, int64_t *n_active);
+/* active0_mode: 0 none (all nonzero-norm columns), 1 host array active0[n0],
+ * 2 the device set left by gs_solver_seq_screen. */
+int gs_solver_solve(gs_solver *S, double lam, const gs_solve_config *cfg, const int64_t *active0,
+                    int64_t n0, int active0_mode, gs_solve_result *res);
+void gs_solver_free(gs_solver *S);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAPSAFE_B200_H */

@@ -1,0 +1,925 @@
+// sm_100a kernels of the Gap Safe Lasso hot path.
+//
+//   k_gemv_t_*      screening / restricted X^T v pass (A2, A4, A5b, A6) with
+//                   fused epilogues: |.|-argmax, sphere test mu >= 1 - tol,
+//                   per-column certification thresholds for the CD kernel.
+//   k_compact_*     stable (ascending) stream compaction of surviving indices.
+//   k_resync_*      residual rho = y - X beta over the support only (A5a).
+//   k_ckpt_*        checkpoint scalar algebra: Eq. 10 dual point, P, D, G,
+//                   radius, drop axpys, post-drop certificate, trace (A5b-d).
+//   k_cd_epoch_*    one cyclic CD epoch over the active set, one CTA per
+//                   problem, with exact certified-zero skipping (A7).
+//   k_*_exact       kernel-level twins of _kernels.py in the reference's own
+//                   summation order (sequential, non-FMA) for bit-exact tests.
+#pragma once
+#include "gs_device.cuh"
+
+namespace gs {
+
+// ---------------------------------------------------------------------------
+// device-resident scalar block of one solve (read back once per checkpoint)
+// ---------------------------------------------------------------------------
+struct DevScalars {
+    // problem
+    double lam, eps, y_norm_sq;
+    // dual point (problem.py:98-123)
+    double rho_sq, y_rho, corr, alpha, margin;
+    int64_t corr_arg;
+    int32_t interp, status;
+    // certificates (problem.py:57-86, regions.py:213-218)
+    double l1, primal, dual, gap_pre, radius, primal_post, gap_post, radius_post;
+    // certification anchor
+    double rho_norm_ub;
+    // counts
+    int64_t m;            // active-set size
+    int64_t cnt;          // generic compaction output count
+    int64_t n_supp;       // support size (resync)
+    int64_t n_drop;       // dropped columns with beta != 0
+    // CD statistics
+    unsigned long long visits, uncertified, nonzero;
+};
+
+enum Status : int32_t {
+    ST_OK = 0,
+    ST_INFEASIBLE = 1,     // InfeasibleDualError   (problem.py:74-76)
+    ST_NEG_GAP = 2,        // NumericalInconsistencyError (regions.py:215-217)
+};
+
+// ---------------------------------------------------------------------------
+// column dot products (warp per column), fixed order, FMA
+// ---------------------------------------------------------------------------
+template <typename T> struct ColDot;
+
+template <> struct ColDot<double> {
+    // ld must be even: column start is 16-B aligned, rows read as double2.
+    static __device__ __forceinline__ double run(const double* __restrict__ x,
+                                                 const double* __restrict__ v, int n, int lane) {
+        const double2* x2 = reinterpret_cast<const double2*>(x);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const int n2 = n >> 1;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n2; q += kWarp) {
+            const double2 xv = __ldg(x2 + q);
+            const double2 vv = v2[q];
+            a0 = fma(xv.x, vv.x, a0);
+            a1 = fma(xv.y, vv.y, a1);
+        }
+        if ((n & 1) && lane == 0) a0 = fma(__ldg(x + n - 1), v[n - 1], a0);
+        return warp_sum(a0 + a1);
+    }
+};
+
+template <> struct ColDot<float> {
+    // ld must be a multiple of 4: rows read as float4.
+    static __device__ __forceinline__ double run(const float* __restrict__ x,
+                                                 const double* __restrict__ v, int n, int lane) {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const int n4 = n >> 2;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n4; q += kWarp) {
+            const float4 xv = __ldg(x4 + q);
+            const double2 va = v2[2 * q], vb = v2[2 * q + 1];
+            a0 = fma((double)xv.x, va.x, a0);
+            a1 = fma((double)xv.y, va.y, a1);
+            a0 = fma((double)xv.z, vb.x, a0);
+            a1 = fma((double)xv.w, vb.y, a1);
+        }
+        for (int r = (n4 << 2) + lane; r < n; r += kWarp) a0 = fma((double)__ldg(x + r), v[r], a0);
+        return warp_sum(a0 + a1);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// screening / restricted GEMV with fused epilogues
+// ---------------------------------------------------------------------------
+enum GemvMode : int {
+    GEMV_RAW = 0,    // out_c[i] = x_{j}^T v
+    GEMV_MAX = 1,    // + per-block max |c| (smallest index on ties)
+    GEMV_MU = 2,     // sphere test: mu = |c| * scale + r * ||x_j||; flags = mu >= thresh
+    GEMV_CERT = 3,   // out_c, per-column certification threshold out_t, + block max
+};
+
+struct GemvArgs {
+    int64_t ld;
+    int n;
+    const double* v;           // [n]
+    const int32_t* cols;       // nullable -> identity (i -> column i)
+    int64_t m;                 // number of columns processed
+    int cpb;                   // columns per block
+    int mode;
+    double* out_c;             // [m] nullable
+    double* blk_val;           // [grid] (MAX, CERT)
+    int64_t* blk_idx;          // [grid]
+    // MU
+    double scale;
+    const double* radius_dev;  // nullable -> radius_host
+    double radius_host;
+    double thresh;             // 1 - tol
+    const double* norms;       // [p] column norms
+    double* out_mu;            // [m] nullable
+    uint8_t* flags;            // [m]
+    // CERT
+    double* out_t;             // [m]
+    const double* beta;        // [p]
+    double lam;
+    const double* rho_norm_dev;
+    double gam;                // gamma_n
+};
+
+// Certification threshold: with
+// c = fl(x^T rho0) and Delta >= ||rho - rho0||, the CD kernel's own dot
+// g = fl(x^T rho) obeys |g| <= |c| + 2 gam ||x|| ||rho0|| + (1+gam)^2 ||x|| Delta,
+// so Delta < t guarantees |g| <= lam, hence z = fl(g/nsq) in [-u, u], hence a
+// zero update (for beta_j == 0).  All operations round toward the safe side.
+__device__ __forceinline__ double cert_threshold(double c, double norm, double lam,
+                                                 double rho0, double gam) {
+    const double k = 1.0 + 4.0 * gam + 1e-13;
+    const double num = __dsub_rd(__dsub_rd(lam, fabs(c)), __dmul_ru(__dmul_ru(2.0 * k, gam), __dmul_ru(norm, rho0)));
+    const double den = __dmul_ru(norm, __dmul_ru(k, k));
+    if (!(num > 0.0)) return -1.0;
+    return __ddiv_rd(num, den);
+}
+
+template <typename T, bool VSMEM>
+__global__ void __launch_bounds__(256) k_gemv_t_dense(const T* __restrict__ X, GemvArgs a) {
+    extern __shared__ double smem_v[];
+    __shared__ double s_val[8];
+    __shared__ int64_t s_idx[8];
+    __shared__ int s_cnt[8];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * a.cpb;
+    const int64_t i1 = min(a.m, i0 + (int64_t)a.cpb);
+    if (VSMEM) {
+        for (int r = tid; r < a.n; r += blockDim.x) smem_v[r] = a.v[r];
+        if (tid == 0 && (a.n & 1)) smem_v[a.n] = 0.0;
+        __syncthreads();
+    }
+    const double* v = VSMEM ? smem_v : a.v;
+    const double radius = (a.mode == GEMV_MU) ? (a.radius_dev ? *a.radius_dev : a.radius_host) : 0.0;
+    const double rho0 = (a.mode == GEMV_CERT) ? *a.rho_norm_dev : 0.0;
+    double bmax = -1.0;
+    int64_t barg = INT64_MAX;
+    int cnt = 0;
+    for (int64_t i = i0 + w; i < i1; i += nw) {
+        const int64_t j = a.cols ? (int64_t)a.cols[i] : i;
+        const double c = ColDot<T>::run(X + j * a.ld, v, a.n, lane);
+        if (lane == 0) {
+            if (a.out_c) a.out_c[i] = c;
+            if (a.mode == GEMV_MAX || a.mode == GEMV_CERT) argmax_merge(bmax, barg, fabs(c), i);
+            if (a.mode == GEMV_MU) {
+                const double mu = fabs(c) * a.scale + radius * a.norms[j];
+                if (a.out_mu) a.out_mu[i] = mu;
+                const bool keep = mu >= a.thresh;
+                a.flags[i] = keep;
+                cnt += keep;
+            } else if (a.mode == GEMV_CERT) {
+                a.out_t[i] = (a.beta[j] != 0.0) ? -1.0 : cert_threshold(c, a.norms[j], a.lam, rho0, a.gam);
+            }
+        }
+    }
+    if (a.mode == GEMV_MAX || a.mode == GEMV_CERT) {
+        if (lane == 0) { s_val[w] = bmax; s_idx[w] = barg; }
+        __syncthreads();
+        if (tid == 0) {
+            for (int k = 1; k < nw; ++k) argmax_merge(bmax, barg, s_val[k], s_idx[k]);
+            a.blk_val[blockIdx.x] = bmax;
+            a.blk_idx[blockIdx.x] = barg;
+        }
+    }
+    (void)s_cnt;
+}
+
+// CSC: warp per column, entries in storage order (sorted rows).
+__global__ void __launch_bounds__(256) k_gemv_t_csc(const double* __restrict__ data,
+                                                    const int32_t* __restrict__ indices,
+                                                    const int64_t* __restrict__ indptr, GemvArgs a) {
+    __shared__ double s_val[8];
+    __shared__ int64_t s_idx[8];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * a.cpb;
+    const int64_t i1 = min(a.m, i0 + (int64_t)a.cpb);
+    const double radius = (a.mode == GEMV_MU) ? (a.radius_dev ? *a.radius_dev : a.radius_host) : 0.0;
+    const double rho0 = (a.mode == GEMV_CERT) ? *a.rho_norm_dev : 0.0;
+    double bmax = -1.0;
+    int64_t barg = INT64_MAX;
+    for (int64_t i = i0 + w; i < i1; i += nw) {
+        const int64_t j = a.cols ? (int64_t)a.cols[i] : i;
+        const int64_t lo = __ldg(indptr + j), hi = __ldg(indptr + j + 1);
+        double acc = 0.0;
+        for (int64_t q = lo + lane; q < hi; q += kWarp)
+            acc = fma(__ldg(data + q), __ldg(a.v + __ldg(indices + q)), acc);
+        const double c = warp_sum(acc);
+        if (lane == 0) {
+            if (a.out_c) a.out_c[i] = c;
+            if (a.mode == GEMV_MAX || a.mode == GEMV_CERT) argmax_merge(bmax, barg, fabs(c), i);
+            if (a.mode == GEMV_MU) {
+                const double mu = fabs(c) * a.scale + radius * a.norms[j];
+                if (a.out_mu) a.out_mu[i] = mu;
+                a.flags[i] = mu >= a.thresh;
+            } else if (a.mode == GEMV_CERT) {
+                a.out_t[i] = (a.beta[j] != 0.0) ? -1.0 : cert_threshold(c, a.norms[j], a.lam, rho0, a.gam);
+            }
+        }
+    }
+    if (a.mode == GEMV_MAX || a.mode == GEMV_CERT) {
+        if (lane == 0) { s_val[w] = bmax; s_idx[w] = barg; }
+        __syncthreads();
+        if (tid == 0) {
+            for (int k = 1; k < nw; ++k) argmax_merge(bmax, barg, s_val[k], s_idx[k]);
+            a.blk_val[blockIdx.x] = bmax;
+            a.blk_idx[blockIdx.x] = barg;
+        }
+    }
+}
+
+// second stage of the block max: one block; writes (max, position) to out.
+__global__ void k_max_finalize(const double* __restrict__ bv, const int64_t* __restrict__ bi,
+                               int64_t nb, double* out_val, int64_t* out_idx) {
+    __shared__ double s_val[32];
+    __shared__ int64_t s_idx[32];
+    double v = -1.0;
+    int64_t i = INT64_MAX;
+    for (int64_t k = threadIdx.x; k < nb; k += blockDim.x) argmax_merge(v, i, bv[k], bi[k]);
+    warp_argmax(v, i);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if (lane == 0) { s_val[w] = v; s_idx[w] = i; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < nw; ++k) argmax_merge(v, i, s_val[k], s_idx[k]);
+        *out_val = v < 0.0 ? 0.0 : v;
+        *out_idx = i == INT64_MAX ? 0 : i;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stable stream compaction (ascending), chunk = 4 elements/thread x 256 threads
+// ---------------------------------------------------------------------------
+constexpr int kCompactChunk = 1024;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int s = lane < nw ? sh[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) sh[lane] = s;
+    }
+    __syncthreads();
+    total = sh[nw - 1];
+    const int excl = (w ? sh[w - 1] : 0) + x - v;
+    __syncthreads();
+    return excl;
+}
+
+__global__ void __launch_bounds__(256) k_compact_count(const uint8_t* __restrict__ flags, int64_t m,
+                                                       int32_t* __restrict__ cnt) {
+    __shared__ int sh[32];
+    const int64_t base = (int64_t)blockIdx.x * kCompactChunk + threadIdx.x * 4;
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c += (base + k < m) ? (int)flags[base + k] : 0;
+    int total;
+    block_excl_scan(c, sh, total);
+    if (threadIdx.x == 0) cnt[blockIdx.x] = total;
+}
+
+// exclusive scan of block counts (one block), writes offsets and total.
+__global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t nb, int64_t* __restrict__ off,
+                              int64_t* total_out) {
+    __shared__ int64_t sh[1024];
+    const int t = threadIdx.x, T = blockDim.x;
+    const int64_t per = (nb + T - 1) / T;
+    const int64_t lo = t * per, hi = min(nb, lo + per);
+    int64_t s = 0;
+    for (int64_t k = lo; k < hi; ++k) s += cnt[k];
+    sh[t] = s;
+    __syncthreads();
+    if (t == 0) {
+        int64_t acc = 0;
+        for (int k = 0; k < T; ++k) { int64_t v = sh[k]; sh[k] = acc; acc += v; }
+        *total_out = acc;
+    }
+    __syncthreads();
+    int64_t acc = sh[t];
+    for (int64_t k = lo; k < hi; ++k) { off[k] = acc; acc += cnt[k]; }
+}
+
+// out[off + rank] = cols ? cols[i] : i, for flagged i in ascending order.
+__global__ void __launch_bounds__(256) k_compact_scatter(const uint8_t* __restrict__ flags, int64_t m,
+                                                         const int32_t* __restrict__ cols,
+                                                         const int64_t* __restrict__ off,
+                                                         int32_t* __restrict__ out) {
+    __shared__ int sh[32];
+    const int64_t base = (int64_t)blockIdx.x * kCompactChunk + threadIdx.x * 4;
+    int f[4], c = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { f[k] = (base + k < m) ? (int)flags[base + k] : 0; c += f[k]; }
+    int total;
+    int pos = block_excl_scan(c, sh, total);
+    const int64_t o = off[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (f[k]) { const int64_t i = base + k; out[o + pos++] = cols ? cols[i] : (int32_t)i; }
+}
+
+// ---------------------------------------------------------------------------
+// small element-wise kernels
+// ---------------------------------------------------------------------------
+__global__ void k_flags_norm_pos(const int32_t* __restrict__ cols, int64_t m, const double* __restrict__ norms,
+                                 uint8_t* __restrict__ flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = cols ? cols[i] : i;
+        flags[i] = norms[j] > 0.0;
+    }
+}
+
+__global__ void k_flags_beta_nz(const int32_t* __restrict__ cols, int64_t m, const double* __restrict__ beta,
+                                uint8_t* __restrict__ flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = cols ? cols[i] : i;
+        flags[i] = beta[j] != 0.0;
+    }
+}
+
+__global__ void k_set_mark(const int32_t* __restrict__ cols, int64_t m, uint8_t* __restrict__ mark) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        mark[cols[i]] = 1;
+}
+
+// beta_j = 0 where mark_j == 0 (solver.py:176-178), then clears mark.
+__global__ void k_zero_unmarked(double* __restrict__ beta, uint8_t* __restrict__ mark, int64_t p) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        if (!mark[j]) beta[j] = 0.0;
+        mark[j] = 0;
+    }
+}
+
+__global__ void k_scale_vec(const double* __restrict__ x, double s, int64_t n, double* __restrict__ out,
+                            int divide) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = divide ? x[i] / s : x[i] * s;
+}
+
+// ---------------------------------------------------------------------------
+// residual resync over the support only (design_matrix.py:130-137 semantics)
+// ---------------------------------------------------------------------------
+// partial[c*n + r] = sum_{k in chunk c} X[r, S[k]] * beta[S[k]]  (ascending k, FMA)
+template <typename T>
+__global__ void __launch_bounds__(256) k_resync_partial_dense(const T* __restrict__ X, int64_t ld, int n,
+                                                              const int32_t* __restrict__ S,
+                                                              const int64_t* __restrict__ s_count,
+                                                              const double* __restrict__ beta, int nchunks,
+                                                              double* __restrict__ partial) {
+    const int64_t s = *s_count;
+    const int c = blockIdx.y;
+    const int64_t per = (s + nchunks - 1) / nchunks;
+    const int64_t k0 = (int64_t)c * per, k1 = min(s, k0 + per);
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double acc = 0.0;
+    for (int64_t k = k0; k < k1; ++k) {
+        const int64_t j = S[k];
+        acc = fma(to_d(__ldg(X + j * ld + r)), beta[j], acc);
+    }
+    partial[(int64_t)c * n + r] = acc;
+}
+
+// out[r] = (y ? y[r] - sum : sum) over chunks in ascending order.
+__global__ void k_resync_final(const double* __restrict__ y, const double* __restrict__ partial, int nchunks,
+                               int n, double* __restrict__ out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += partial[(int64_t)c * n + r];
+    out[r] = y ? y[r] - s : s;
+}
+
+// CSR row products: out[r] = (y ? y[r] - sum : sum), sum over the row in column order.
+__global__ void k_resync_csr(const double* __restrict__ data, const int32_t* __restrict__ cols,
+                             const int64_t* __restrict__ rowptr, int n, const double* __restrict__ beta,
+                             const double* __restrict__ y, double* __restrict__ out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double s = 0.0;
+    for (int64_t q = rowptr[r]; q < rowptr[r + 1]; ++q) s = fma(data[q], beta[cols[q]], s);
+    out[r] = y ? y[r] - s : s;
+}
+
+// ---------------------------------------------------------------------------
+// checkpoint scalar algebra (single block)
+// ---------------------------------------------------------------------------
+// Eq. 10 dual point and pre-drop certificate (problem.py:98-123, 57-86;
+// regions.py:213-218).  restricted m = |X_A^T rho|_inf arrives in sc->corr.
+__global__ void __launch_bounds__(1024) k_ckpt_dual(const double* __restrict__ rho, const double* __restrict__ y,
+                                                    int n, const double* __restrict__ beta,
+                                                    const int32_t* __restrict__ A, int64_t m,
+                                                    double* __restrict__ theta, DevScalars* sc, int want_radius) {
+    __shared__ double red[32];
+    const double lam = sc->lam;
+    double a = 0.0, b = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) { const double q = rho[r]; a = fma(q, q, a); b = fma(y[r], q, b); }
+    const double rho_sq = block_sum(a, red);
+    const double y_rho = block_sum(b, red);
+    const double corr = sc->corr;
+    double alpha = 0.0, margin = 1.0;
+    int interp = 0;
+    if (rho_sq == 0.0) {
+        interp = 1;
+    } else {
+        const double raw = y_rho / (lam * rho_sq);
+        if (corr > 0.0) {
+            const double bound = 1.0 / corr;
+            alpha = fmin(fmax(raw, -bound), bound);
+        } else {
+            alpha = raw;
+        }
+        margin = 1.0 - fabs(alpha) * corr;
+    }
+    double dd = 0.0, l1 = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const double th = interp ? 0.0 : alpha * rho[r];
+        theta[r] = th;
+        const double diff = th - y[r] / lam;
+        dd = fma(diff, diff, dd);
+    }
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) l1 += fabs(beta[A[i]]);
+    const double dsq = block_sum(dd, red);
+    const double l1s = block_sum(l1, red);
+    if (threadIdx.x == 0) {
+        const double dual = 0.5 * sc->y_norm_sq - 0.5 * (lam * lam) * dsq;
+        const double primal = 0.5 * rho_sq + lam * l1s;
+        const double gap = primal - dual;
+        sc->rho_sq = rho_sq; sc->y_rho = y_rho; sc->alpha = alpha; sc->margin = margin; sc->interp = interp;
+        sc->l1 = l1s; sc->primal = primal; sc->dual = dual; sc->gap_pre = gap;
+        int st = ST_OK;
+        if (margin < -1e-9) st = ST_INFEASIBLE;
+        else if (want_radius && gap < -1e-10) st = ST_NEG_GAP;
+        sc->status = st;
+        sc->radius = sqrt(2.0 * fmax(gap, 0.0)) / lam;
+    }
+}
+
+// mu_A from the stored restricted dots: mu_i = |alpha c_i| + r ||x_{A_i}||,
+// keep = mu >= 1 - tol (solver.py:208-209); drop_nz = !keep && beta != 0.
+__global__ void k_ckpt_keep(const double* __restrict__ c, const int32_t* __restrict__ A, int64_t m,
+                            const double* __restrict__ norms, const double* __restrict__ beta,
+                            const DevScalars* __restrict__ sc, double thresh,
+                            uint8_t* __restrict__ keep, uint8_t* __restrict__ drop_nz) {
+    const double alpha = sc->alpha, r = sc->radius;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = A[i];
+        const double mu = fabs(alpha * c[i]) + r * norms[j];
+        const bool k = mu >= thresh;
+        keep[i] = k;
+        drop_nz[i] = (!k) && beta[j] != 0.0;
+    }
+}
+
+// rho += beta_j x_j for dropped j in ascending order (numpy: v += a * x,
+// separate roundings), thread per row.
+template <typename T>
+__global__ void k_drop_axpy_dense(const T* __restrict__ X, int64_t ld, int n, const int32_t* __restrict__ D,
+                                  const int64_t* __restrict__ d_count, const double* __restrict__ beta,
+                                  double* __restrict__ rho) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nd = *d_count;
+    if (r >= n || nd == 0) return;
+    double q = rho[r];
+    for (int64_t k = 0; k < nd; ++k) {
+        const int64_t j = D[k];
+        q = __dadd_rn(q, __dmul_rn(beta[j], to_d(X[j * ld + r])));
+    }
+    rho[r] = q;
+}
+
+// CSC variant: one block, columns in ascending order, a barrier between
+// columns (rows inside one column are distinct).
+__global__ void k_drop_axpy_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
+                                const int64_t* __restrict__ indptr, const int32_t* __restrict__ D,
+                                const int64_t* __restrict__ d_count, const double* __restrict__ beta,
+                                double* __restrict__ rho) {
+    const int64_t nd = *d_count;
+    for (int64_t k = 0; k < nd; ++k) {
+        const int64_t j = D[k];
+        const double bj = beta[j];
+        for (int64_t q = indptr[j] + threadIdx.x; q < indptr[j + 1]; q += blockDim.x)
+            rho[indices[q]] = __dadd_rn(rho[indices[q]], __dmul_rn(bj, data[q]));
+        __syncthreads();
+    }
+}
+
+__global__ void k_zero_listed(double* __restrict__ beta, const int32_t* __restrict__ D,
+                              const int64_t* __restrict__ d_count) {
+    const int64_t nd = *d_count;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nd; k += (int64_t)gridDim.x * blockDim.x)
+        beta[D[k]] = 0.0;
+}
+
+// post-drop certificate with the same theta (solver.py:217-221), trace row.
+struct TraceRow { int64_t passes, n_active; double gap, radius; };
+
+__global__ void __launch_bounds__(1024) k_ckpt_post(const double* __restrict__ rho, int n,
+                                                    const double* __restrict__ beta,
+                                                    const int32_t* __restrict__ A, DevScalars* sc,
+                                                    TraceRow* trace, int64_t trace_pos, int64_t passes) {
+    __shared__ double red[32];
+    const double lam = sc->lam;
+    const int64_t m = sc->m;
+    double a = 0.0, aru = 0.0, l1 = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) { const double q = rho[r]; a = fma(q, q, a); aru = __dadd_ru(aru, __dmul_ru(q, q)); }
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) l1 += fabs(beta[A[i]]);
+    const double rho_sq = block_sum(a, red);
+    const double rho_sq_ru = block_sum_ru(aru, red);
+    const double l1s = block_sum(l1, red);
+    if (threadIdx.x == 0) {
+        const double primal = 0.5 * rho_sq + lam * l1s;
+        const double gap = primal - sc->dual;
+        sc->primal_post = primal;
+        sc->gap_post = gap;
+        sc->radius_post = sqrt(2.0 * fmax(gap, 0.0)) / lam;
+        sc->rho_norm_ub = __dsqrt_ru(rho_sq_ru);
+        if (trace) trace[trace_pos] = TraceRow{passes, m, gap, sc->radius_post};
+    }
+}
+
+// rigorous upper bound of ||rho|| (certification anchor after a resync).
+__global__ void __launch_bounds__(1024) k_rho_norm_ub(const double* __restrict__ rho, int n, DevScalars* sc) {
+    __shared__ double red[32];
+    double a = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) { const double q = rho[r]; a = __dadd_ru(a, __dmul_ru(q, q)); }
+    const double s = block_sum_ru(a, red);
+    if (threadIdx.x == 0) sc->rho_norm_ub = __dsqrt_ru(s);
+}
+
+// generic dot / abs-sum over device vectors (problem.py scalar algebra for
+// the drop-in helper functions).  out[0] = sum a*b, out[1] = sum |a|.
+__global__ void __launch_bounds__(1024) k_vec_stats(const double* __restrict__ a, const double* __restrict__ b,
+                                                    int64_t n, double* out) {
+    __shared__ double red[32];
+    double s = 0.0, t = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = a[i];
+        if (b) s = fma(x, b[i], s);
+        t += fabs(x);
+    }
+    s = block_sum(s, red);
+    t = block_sum(t, red);
+    if (threadIdx.x == 0) { out[0] = s; out[1] = t; }
+}
+
+// sequential-screen gap at a new lambda for the previous pair (path.py:82-91,
+// regions.py:221-232).  Reads previous beta over the previous active set.
+__global__ void __launch_bounds__(1024) k_seq_gap(const double* __restrict__ rho, const double* __restrict__ y,
+                                                  const double* __restrict__ theta, int n,
+                                                  const double* __restrict__ beta, const int32_t* __restrict__ A,
+                                                  int64_t m, double prev_margin, DevScalars* sc) {
+    __shared__ double red[32];
+    const double lam = sc->lam;
+    double a = 0.0, dd = 0.0, l1 = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const double q = rho[r];
+        a = fma(q, q, a);
+        const double diff = theta[r] - y[r] / lam;
+        dd = fma(diff, diff, dd);
+    }
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) l1 += fabs(beta[A[i]]);
+    const double rho_sq = block_sum(a, red);
+    const double dsq = block_sum(dd, red);
+    const double l1s = block_sum(l1, red);
+    if (threadIdx.x == 0) {
+        const double primal = 0.5 * rho_sq + lam * l1s;
+        const double dual = 0.5 * sc->y_norm_sq - 0.5 * (lam * lam) * dsq;
+        const double gap = primal - dual;
+        int st = ST_OK;
+        if (prev_margin < -1e-9) st = ST_INFEASIBLE;
+        else if (gap < -1e-10) st = ST_NEG_GAP;
+        sc->status = st;
+        sc->gap_pre = gap;
+        sc->radius = sqrt(2.0 * fmax(gap, 0.0)) / lam;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CD epoch, dense, one CTA per problem (solver.py:82-101, _kernels.py:39-64)
+// ---------------------------------------------------------------------------
+// Thread t owns rows t, t+B, ..., t+(R-1)B of rho in registers.  For each
+// active column in ascending order the CTA either
+//   * skips it: certified zero update (t_i > Delta, see cert_threshold), which
+//     is bit-exact with computing it, or
+//   * computes g = x^T rho (thread FMA chain over its rows, warp butterfly,
+//     warps summed in order), z = beta + g/nsq, u = lam/nsq, soft threshold,
+//     and on d != 0 updates beta and rho -= d*x with separate roundings.
+// Delta (rigorous, round-up) bounds ||rho - rho0|| since the anchor rho0 at
+// which t was computed.  tcert == nullptr disables skipping.
+struct CdArgs {
+    int64_t ld;
+    int n;
+    const int32_t* A;
+    int64_t m;
+    const double* tcert;
+    double* beta;
+    double* rho;
+    const double* nsq;
+    const double* norms;
+    double lam;
+    DevScalars* sc;
+};
+
+__device__ __forceinline__ int64_t cd_next_uncertified(const double* __restrict__ tcert, int64_t pos, int64_t m,
+                                                       double Delta, int* s_first, int& phase) {
+    if (!tcert) return pos;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    while (pos < m) {
+        const int64_t i = pos + threadIdx.x;
+        const bool unc = (i < m) && !(Delta < tcert[i]);
+        const unsigned bal = __ballot_sync(0xffffffffu, unc);
+        int* sf = s_first + phase * 32;
+        if (lane == 0) sf[w] = bal ? (w * 32 + __ffs(bal) - 1) : INT32_MAX;
+        __syncthreads();
+        int f = INT32_MAX;
+        for (int k = 0; k < nw; ++k) f = min(f, sf[k]);
+        phase ^= 1;
+        if (f != INT32_MAX) return pos + f;
+        pos += blockDim.x;
+    }
+    return m;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(R >= 8 ? 512 : 1024) k_cd_epoch_dense(const T* __restrict__ X, CdArgs a) {
+    __shared__ double s_part[2][32];
+    __shared__ int s_first[2 * 32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5, B = blockDim.x;
+    double rr[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) { const int r = tid + k * B; rr[k] = r < a.n ? a.rho[r] : 0.0; }
+    const double rho0 = a.sc->rho_norm_ub;
+    const double lam = a.lam;
+    double Delta = 0.0;
+    int pbuf = 0, phase = 0;
+    unsigned long long n_unc = 0, n_nz = 0;
+    int64_t pos = 0;
+    while (true) {
+        const int64_t i = cd_next_uncertified(a.tcert, pos, a.m, Delta, s_first, phase);
+        if (i >= a.m) break;
+        const int64_t j = a.A[i];
+        const T* x = X + j * a.ld;
+        double xv[R];
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int r = tid + k * B;
+            xv[k] = r < a.n ? to_d(__ldg(x + r)) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc = fma(xv[k], rr[k], acc);
+        // every thread reads beta_j before the barrier; thread 0 writes it after
+        const double bj = a.beta[j];
+        const double nsq = a.nsq[j];
+        acc = warp_sum(acc);
+        if (lane == 0) s_part[pbuf][w] = acc;
+        __syncthreads();
+        double g = 0.0;
+        for (int k = 0; k < nw; ++k) g += s_part[pbuf][k];
+        pbuf ^= 1;
+        const double z = bj + g / nsq;
+        const double u = lam / nsq;
+        const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+        const double d = nb - bj;
+        ++n_unc;
+        if (d != 0.0) {
+            ++n_nz;
+            if (tid == 0) a.beta[j] = nb;
+#pragma unroll
+            for (int k = 0; k < R; ++k) rr[k] = __dsub_rn(rr[k], __dmul_rn(d, xv[k]));
+            const double step = __dmul_ru(fabs(d), a.norms[j]);
+            Delta = __dadd_ru(Delta, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12),
+                                               __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, Delta), step))));
+        }
+        pos = i + 1;
+    }
+    // write back rho and a rigorous ||rho|| bound for the next anchor
+    __shared__ double red[32];
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int r = tid + k * B;
+        if (r < a.n) { a.rho[r] = rr[k]; s = __dadd_ru(s, __dmul_ru(rr[k], rr[k])); }
+    }
+    s = block_sum_ru(s, red);
+    if (tid == 0) {
+        a.sc->rho_norm_ub = __dsqrt_ru(s);
+        a.sc->visits += (unsigned long long)a.m;
+        a.sc->uncertified += n_unc;
+        a.sc->nonzero += n_nz;
+    }
+    (void)lane;
+}
+
+// CSC: rho in shared memory; every warp computes the same column dot
+// redundantly (lane-strided over the column's entries, butterfly), so d and
+// Delta are known CTA-wide without an extra barrier; warp 0 applies updates.
+__global__ void __launch_bounds__(1024) k_cd_epoch_csc(const double* __restrict__ data,
+                                                       const int32_t* __restrict__ indices,
+                                                       const int64_t* __restrict__ indptr, CdArgs a) {
+    extern __shared__ double s_rho[];
+    __shared__ int s_first[2 * 32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int r = tid; r < a.n; r += blockDim.x) s_rho[r] = a.rho[r];
+    __syncthreads();
+    const double rho0 = a.sc->rho_norm_ub;
+    const double lam = a.lam;
+    double Delta = 0.0;
+    int phase = 0;
+    unsigned long long n_unc = 0, n_nz = 0;
+    int64_t pos = 0;
+    while (true) {
+        const int64_t i = cd_next_uncertified(a.tcert, pos, a.m, Delta, s_first, phase);
+        if (!a.tcert) __syncthreads();   // order the previous step's rho writes
+        if (i >= a.m) break;
+        const int64_t j = a.A[i];
+        const int64_t lo = indptr[j], hi = indptr[j + 1];
+        const double bj = a.beta[j];
+        const double nsq = a.nsq[j];
+        double acc = 0.0;
+        for (int64_t q = lo + lane; q < hi; q += kWarp) acc = fma(__ldg(data + q), s_rho[__ldg(indices + q)], acc);
+        const double g = warp_sum(acc);
+        const double z = bj + g / nsq;
+        const double u = lam / nsq;
+        const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+        const double d = nb - bj;
+        ++n_unc;
+        if (d != 0.0) {
+            ++n_nz;
+            __syncthreads();   // d is CTA-uniform: all warps finished reading rho and beta_j
+            if (w == 0) {
+                if (lane == 0) a.beta[j] = nb;
+                for (int64_t q = lo + lane; q < hi; q += kWarp) {
+                    const int32_t r = __ldg(indices + q);
+                    s_rho[r] = __dsub_rn(s_rho[r], __dmul_rn(d, __ldg(data + q)));
+                }
+            }
+            const double step = __dmul_ru(fabs(d), a.norms[j]);
+            Delta = __dadd_ru(Delta, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12),
+                                               __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, Delta), step))));
+        }
+        pos = i + 1;
+    }
+    __syncthreads();
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int r = tid; r < a.n; r += blockDim.x) { const double q = s_rho[r]; a.rho[r] = q; s = __dadd_ru(s, __dmul_ru(q, q)); }
+    s = block_sum_ru(s, red);
+    if (tid == 0) {
+        a.sc->rho_norm_ub = __dsqrt_ru(s);
+        a.sc->visits += (unsigned long long)a.m;
+        a.sc->uncertified += n_unc;
+        a.sc->nonzero += n_nz;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact-order kernel twins (reference summation order, for bit-exact tests)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_tdot_exact_dense(const T* __restrict__ X, int64_t ld, int n, const double* __restrict__ v,
+                                   const int32_t* __restrict__ cols, int64_t k, double tail_scale,
+                                   double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = cols[i];
+        const T* x = X + j * ld;
+        double s = 0.0;
+        for (int r = 0; r < n; ++r) s = __dadd_rn(s, __dmul_rn(to_d(x[r]), v[r]));
+        if (tail_scale > 0.0) s = __dadd_rn(s, __dmul_rn(tail_scale, v[n + j]));
+        out[i] = s;
+    }
+}
+
+__global__ void k_tdot_exact_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
+                                 const int64_t* __restrict__ indptr, int n, const double* __restrict__ v,
+                                 const int32_t* __restrict__ cols, int64_t k, double tail_scale,
+                                 double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = cols[i];
+        double s = 0.0;
+        for (int64_t q = indptr[j]; q < indptr[j + 1]; ++q) s = __dadd_rn(s, __dmul_rn(data[q], v[indices[q]]));
+        if (tail_scale > 0.0) s = __dadd_rn(s, __dmul_rn(tail_scale, v[n + j]));
+        out[i] = s;
+    }
+}
+
+// one block: thread 0 forms the sequential non-FMA dot, all threads apply the
+// axpy with separate roundings (_kernels.py:39-92 arithmetic, bit for bit).
+template <typename T>
+__global__ void k_cd_pass_exact_dense(const T* __restrict__ X, int64_t ld, int n, double* __restrict__ beta,
+                                      double* __restrict__ rho, const int32_t* __restrict__ A, int64_t k,
+                                      double lam, const double* __restrict__ nsq, double tail_scale) {
+    __shared__ double s_d;
+    for (int64_t i = 0; i < k; ++i) {
+        const int64_t j = A[i];
+        const T* x = X + j * ld;
+        if (threadIdx.x == 0) {
+            double g = 0.0;
+            for (int r = 0; r < n; ++r) g = __dadd_rn(g, __dmul_rn(to_d(x[r]), rho[r]));
+            if (tail_scale > 0.0) g = __dadd_rn(g, __dmul_rn(tail_scale, rho[n + j]));
+            const double z = __dadd_rn(beta[j], __ddiv_rn(g, nsq[j]));
+            const double u = __ddiv_rn(lam, nsq[j]);
+            const double nb = z > u ? __dsub_rn(z, u) : (z < -u ? __dadd_rn(z, u) : 0.0);
+            const double d = __dsub_rn(nb, beta[j]);
+            if (d != 0.0) beta[j] = nb;
+            s_d = d;
+        }
+        __syncthreads();
+        const double d = s_d;
+        if (d != 0.0) {
+            for (int r = threadIdx.x; r < n; r += blockDim.x) rho[r] = __dsub_rn(rho[r], __dmul_rn(d, to_d(x[r])));
+            if (tail_scale > 0.0 && threadIdx.x == 0) rho[n + j] = __dsub_rn(rho[n + j], __dmul_rn(d, tail_scale));
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_cd_pass_exact_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
+                                    const int64_t* __restrict__ indptr, int n, double* __restrict__ beta,
+                                    double* __restrict__ rho, const int32_t* __restrict__ A, int64_t k, double lam,
+                                    const double* __restrict__ nsq, double tail_scale) {
+    __shared__ double s_d;
+    for (int64_t i = 0; i < k; ++i) {
+        const int64_t j = A[i];
+        const int64_t lo = indptr[j], hi = indptr[j + 1];
+        if (threadIdx.x == 0) {
+            double g = 0.0;
+            for (int64_t q = lo; q < hi; ++q) g = __dadd_rn(g, __dmul_rn(data[q], rho[indices[q]]));
+            if (tail_scale > 0.0) g = __dadd_rn(g, __dmul_rn(tail_scale, rho[n + j]));
+            const double z = __dadd_rn(beta[j], __ddiv_rn(g, nsq[j]));
+            const double u = __ddiv_rn(lam, nsq[j]);
+            const double nb = z > u ? __dsub_rn(z, u) : (z < -u ? __dadd_rn(z, u) : 0.0);
+            const double d = __dsub_rn(nb, beta[j]);
+            if (d != 0.0) beta[j] = nb;
+            s_d = d;
+        }
+        __syncthreads();
+        const double d = s_d;
+        if (d != 0.0) {
+            for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x)
+                rho[indices[q]] = __dsub_rn(rho[indices[q]], __dmul_rn(d, data[q]));
+            if (tail_scale > 0.0 && threadIdx.x == 0) rho[n + j] = __dsub_rn(rho[n + j], __dmul_rn(d, tail_scale));
+        }
+        __syncthreads();
+    }
+}
+
+// column norms: warp per column, FMA, ascending rows per lane then butterfly.
+template <typename T>
+__global__ void __launch_bounds__(256) k_col_norms_sq_dense(const T* __restrict__ X, int64_t ld, int n, int64_t p,
+                                                            double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = wg; j < p; j += nwg) {
+        const T* x = X + j * ld;
+        double a = 0.0;
+        for (int r = lane; r < n; r += kWarp) { const double q = to_d(__ldg(x + r)); a = fma(q, q, a); }
+        a = warp_sum(a);
+        if (lane == 0) out[j] = a;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_col_norms_sq_csc(const double* __restrict__ data,
+                                                          const int64_t* __restrict__ indptr, int64_t p,
+                                                          double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = wg; j < p; j += nwg) {
+        double a = 0.0;
+        for (int64_t q = indptr[j] + lane; q < indptr[j + 1]; q += kWarp) { const double v = data[q]; a = fma(v, v, a); }
+        a = warp_sum(a);
+        if (lane == 0) out[j] = a;
+    }
+}
+
+__global__ void k_sqrt_vec(const double* __restrict__ a, double add, int64_t p, double* __restrict__ out_sq,
+                           double* __restrict__ out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
+        const double s = a[j] + add;
+        out_sq[j] = s;
+        out[j] = sqrt(s);
+    }
+}
+
+}  // namespace gs

@@ -1,0 +1,200 @@
+"""Device-resident design matrix (drop-in for gapsafe.design_matrix.DesignMatrix,
+/root/reference/pkg/src/gapsafe/design_matrix.py:22-187).
+
+Storage is uploaded once to HBM: dense input as column-major fp64 (or fp32
+storage with fp64 arithmetic, for float32 inputs), sparse input as canonical
+CSC (sorted, deduplicated; design_matrix.py:37-43) plus a CSR copy for the
+row-parallel residual resync.  Column norms are computed on the device.  Every
+method runs a CUDA kernel through the C ABI; host arrays are only the
+caller's inputs and outputs.
+
+Not in this build: the Elastic-Net implicit tail
+(``tail_weight > 0``) raises ``NotImplementedError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+
+
+class DesignMatrix:
+    """n x p feature matrix with cached per-column Euclidean norms."""
+
+    def __init__(self, storage, tail_weight: float = 0.0):
+        if tail_weight < 0:
+            raise ValueError("tail_weight must be non-negative")
+        if tail_weight > 0:
+            raise NotImplementedError(
+                "Elastic-Net implicit tail (tail_weight > 0) is a 'next' row (SURVEY.md §8(f) F2) "
+                "and not part of this build")
+        lib = _lib.load()
+        handle = ctypes.c_void_p()
+        if sp.issparse(storage):
+            mat = sp.csc_matrix(storage).astype(np.float64)
+            mat.sum_duplicates()
+            mat.sort_indices()
+            self._mat = mat
+            self.is_sparse = True
+            self.n_base, self.n_cols = mat.shape
+            if self.n_base < 1 or self.n_cols < 1:
+                raise ValueError("matrix must have at least one row and column")
+            self._indptr64 = np.ascontiguousarray(mat.indptr, dtype=np.int64)
+            data = np.ascontiguousarray(mat.data, dtype=np.float64)
+            indices = np.ascontiguousarray(mat.indices, dtype=np.int32)
+            _lib.check(lib.gs_matrix_csc(_lib.f64p(data), _lib.i32p(indices), _lib.i64p(self._indptr64),
+                                         self.n_base, self.n_cols, None, ctypes.byref(handle)))
+            self.dtype = np.float64
+        else:
+            arr = np.asarray(storage)
+            if arr.dtype != np.float32:
+                arr = np.asarray(arr, dtype=np.float64)
+            arr = np.asfortranarray(arr)
+            if arr.ndim != 2:
+                raise ValueError("storage must be 2-dimensional")
+            self._mat = arr
+            self.is_sparse = False
+            self.n_base, self.n_cols = arr.shape
+            if self.n_base < 1 or self.n_cols < 1:
+                raise ValueError("matrix must have at least one row and column")
+            self.dtype = arr.dtype.type
+            dt = _lib.GS_DTYPE_F32 if arr.dtype == np.float32 else _lib.GS_DTYPE_F64
+            _lib.check(lib.gs_matrix_dense(arr.ctypes.data_as(ctypes.c_void_p), dt, self.n_base,
+                                           self.n_cols, self.n_base, None, ctypes.byref(handle)))
+        self._h = handle
+        self._lib = lib
+        self.tail_weight = 0.0
+        self.tail_scale = 0.0
+        nsq = np.empty(self.n_cols, dtype=np.float64)
+        _lib.check(lib.gs_matrix_norms_sq(self._h, _lib.f64p(nsq)))
+        self._col_norms_sq = nsq
+        self._col_norms = np.sqrt(nsq)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.gs_matrix_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self._lib.gs_matrix_device_bytes(self._h))
+
+    # ------------------------------------------------------------------
+    @property
+    def n_rows(self) -> int:
+        return self.n_base
+
+    @property
+    def col_norms(self) -> np.ndarray:
+        return self._col_norms
+
+    @property
+    def col_norms_sq(self) -> np.ndarray:
+        return self._col_norms_sq
+
+    @property
+    def zero_norm_cols(self) -> np.ndarray:
+        return np.flatnonzero(self._col_norms == 0.0)
+
+    def with_tail(self, tail_weight: float) -> "DesignMatrix":
+        return DesignMatrix(self._mat, tail_weight=tail_weight)
+
+    def normalized(self) -> "DesignMatrix":
+        """Copy with unit-norm columns (zero columns left untouched)."""
+        norms = self._col_norms.copy()
+        norms[norms == 0.0] = 1.0
+        if self.is_sparse:
+            return DesignMatrix(self._mat @ sp.diags(1.0 / norms))
+        return DesignMatrix(self._mat / norms)
+
+    # ------------------------------------------------------------------
+    def _check_col(self, j: int) -> None:
+        if not 0 <= j < self.n_cols:
+            raise IndexError(f"column index {j} out of range [0, {self.n_cols})")
+
+    def _vec(self, v) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.shape != (self.n_rows,):
+            raise ValueError("vector length does not match n_rows")
+        return v
+
+    def col_dot(self, j: int, v: np.ndarray) -> float:
+        """x_j^T v (design_matrix.py:100-113)."""
+        self._check_col(j)
+        return float(self.transpose_dot(v, cols=np.array([j], dtype=np.int64))[0])
+
+    def axpy_col(self, j: int, a: float, v: np.ndarray) -> None:
+        """In place v += a x_j (design_matrix.py:115-128)."""
+        self._check_col(j)
+        if v.shape != (self.n_rows,):
+            raise ValueError("vector length does not match n_rows")
+        if a == 0.0:
+            return
+        buf = np.ascontiguousarray(v, dtype=np.float64)
+        _lib.check(self._lib.gs_axpy_col(self._h, int(j), float(a), _lib.f64p(buf)))
+        if buf is not v:
+            v[...] = buf
+
+    def matvec(self, beta: np.ndarray) -> np.ndarray:
+        """X @ beta (design_matrix.py:130-137)."""
+        beta = np.ascontiguousarray(beta, dtype=np.float64)
+        if beta.shape != (self.n_cols,):
+            raise ValueError("beta has wrong length")
+        out = np.empty(self.n_rows, dtype=np.float64)
+        _lib.check(self._lib.gs_matvec(self._h, _lib.f64p(beta), _lib.f64p(out)))
+        return out
+
+    def transpose_dot(self, v: np.ndarray, cols: np.ndarray | None = None,
+                      exact_order: bool = False) -> np.ndarray:
+        """X^T v, optionally restricted to ``cols`` (design_matrix.py:139-158).
+
+        ``exact_order`` selects the reference kernels' sequential non-FMA
+        summation (bit-exact with _kernels.tdot_*)."""
+        v = self._vec(v)
+        if cols is None:
+            out = np.empty(self.n_cols, dtype=np.float64)
+            _lib.check(self._lib.gs_tdot(self._h, _lib.f64p(v), None, 0, 0.0, _lib.f64p(out),
+                                         int(exact_order)))
+            return out
+        cols = np.ascontiguousarray(cols, dtype=np.int64)
+        out = np.empty(cols.size, dtype=np.float64)
+        if cols.size:
+            _lib.check(self._lib.gs_tdot(self._h, _lib.f64p(v), _lib.i64p(cols), cols.size, 0.0,
+                                         _lib.f64p(out), int(exact_order)))
+        return out
+
+    def max_abs_correlation(self, v: np.ndarray,
+                            restrict: np.ndarray | None = None) -> tuple[float, int]:
+        """(max_j |x_j^T v|, argmax j), ties to the smallest index (:160-174)."""
+        v = self._vec(v)
+        val = ctypes.c_double()
+        arg = ctypes.c_int64()
+        if restrict is not None:
+            restrict = np.ascontiguousarray(restrict, dtype=np.int64)
+            if restrict.size == 0:
+                raise ValueError("empty restriction set")
+            _lib.check(self._lib.gs_max_abs_correlation(self._h, _lib.f64p(v), _lib.i64p(restrict),
+                                                        restrict.size, ctypes.byref(val),
+                                                        ctypes.byref(arg)))
+        else:
+            _lib.check(self._lib.gs_max_abs_correlation(self._h, _lib.f64p(v), None, 0,
+                                                        ctypes.byref(val), ctypes.byref(arg)))
+        return float(val.value), int(arg.value)
+
+    # ------------------------------------------------------------------
+    def toarray(self) -> np.ndarray:
+        base = self._mat.toarray() if self.is_sparse else np.array(self._mat, dtype=np.float64)
+        return np.asfortranarray(base)
+
+    def raw(self):
+        """Host storage handle (the uploaded copy lives on the device)."""
+        return self._mat

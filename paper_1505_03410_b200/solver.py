@@ -1,0 +1,237 @@
+"""Coordinate descent with interlaced Gap Safe screening (drop-in for
+gapsafe.solver, /root/reference/pkg/src/gapsafe/solver.py:1-246).
+
+``solve`` runs Algorithm 1 on the device: residual resync, Eq. 10 dual point
+with the restricted infinity norm, pre-drop gap, sphere test, drop axpys,
+post-drop certificate and trace at every checkpoint, and the CD epochs in
+between (one CTA per problem, exact certified-zero skipping).  The host only
+sequences launches and reads one scalar block per checkpoint.
+
+Rules on the GPU: ``none`` and ``gap_sphere`` (the north_star path).  The
+other members of ``Rule`` exist so configurations validate exactly as in the
+reference, but solving with them raises ``NotImplementedError`` (SURVEY.md
+§8(f) F1/F4 are the "next" rows).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .problem import DualPoint, GapCertificate, LassoProblem
+
+
+class Rule(str, enum.Enum):
+    """Screening rule used at solver checkpoints (solver.py:24-32)."""
+
+    NONE = "none"
+    STATIC = "static"
+    DYNAMIC = "dynamic"
+    ST3 = "st3"
+    GAP_SPHERE = "gap_sphere"
+    GAP_DOME = "gap_dome"
+
+
+_GPU_RULES = {Rule.NONE: _lib.GS_RULE_NONE, Rule.GAP_SPHERE: _lib.GS_RULE_GAP_SPHERE}
+
+
+@dataclass
+class SolverConfig:
+    """solver.py:35-54 (same fields, defaults and validation)."""
+
+    epsilon: float = 1e-8
+    max_passes: int = 10_000
+    screen_every: int = 10
+    rule: Rule = Rule.GAP_SPHERE
+    track_active: bool = False
+    on_checkpoint: object = None
+    # B200 extra: exact certified-zero skipping inside the CD epoch
+    certify: bool = True
+
+    def __post_init__(self):
+        self.rule = Rule(self.rule)
+        if self.epsilon <= 0:
+            raise ValueError("epsilon must be positive")
+        if self.screen_every < 1:
+            raise ValueError("screen_every must be at least 1")
+        if self.max_passes < 1:
+            raise ValueError("max_passes must be at least 1")
+
+
+@dataclass
+class SolverState:
+    """solver.py:57-68."""
+
+    beta: np.ndarray
+    residual: np.ndarray
+    active: np.ndarray
+    theta: DualPoint | None
+    cert: GapCertificate | None
+    passes_done: int
+    converged: bool
+    screen_trace: list = field(default_factory=list)
+    active_history: list = field(default_factory=list)
+    # B200 extras: CD work counters and device time of the solve
+    stats: dict = field(default_factory=dict)
+
+
+def soft_threshold(u: float, x: float) -> float:
+    """sign(x) (|x| - u)_+ (solver.py:71-79)."""
+    if u < 0:
+        raise ValueError("threshold must be non-negative")
+    if x > u:
+        return x - u
+    if x < -u:
+        return x + u
+    return 0.0
+
+
+def cd_pass(state: SolverState, prob: LassoProblem, order: np.ndarray | None = None,
+            exact_order: bool = False) -> SolverState:
+    """One cyclic CD pass over the active set, in place (solver.py:82-90).
+
+    ``exact_order`` runs the reference's sequential non-FMA arithmetic
+    (bit-exact with _kernels.cd_pass_*); otherwise the production kernel."""
+    active = state.active if order is None else np.asarray(order, dtype=np.int64)
+    active = np.ascontiguousarray(active, dtype=np.int64)
+    X = prob.X
+    if np.any(X.col_norms[active] == 0.0):
+        raise RuntimeError("zero-norm column in active set")
+    beta = np.ascontiguousarray(state.beta, dtype=np.float64)
+    rho = np.ascontiguousarray(state.residual, dtype=np.float64)
+    _lib.check(X._lib.gs_cd_pass(X.handle, _lib.f64p(beta), _lib.f64p(rho), _lib.i64p(active),
+                                 active.size, float(prob.lam), None, 0.0, int(exact_order)))
+    if beta is not state.beta:
+        state.beta[...] = beta
+    if rho is not state.residual:
+        state.residual[...] = rho
+    state.passes_done += 1
+    return state
+
+
+class DeviceSolver:
+    """One device solver handle for a fixed (X, y): y, beta, rho, theta and
+    the active set stay resident in HBM across solves (warm starts and the
+    sequential screen of run_path never cross PCIe)."""
+
+    def __init__(self, X, y: np.ndarray):
+        self.X = X
+        self.y = np.ascontiguousarray(y, dtype=np.float64)
+        if self.y.shape != (X.n_rows,):
+            raise ValueError(f"y has length {self.y.shape}, expected ({X.n_rows},)")
+        self._lib = X._lib
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.gs_solver_create(X.handle, _lib.f64p(self.y), ctypes.byref(h)))
+        self._h = h
+        lm, js, yn = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        _lib.check(self._lib.gs_solver_lambda_max(h, ctypes.byref(lm), ctypes.byref(js), ctypes.byref(yn)))
+        self.lambda_max, self.j_star, self.y_norm_sq = lm.value, js.value, yn.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.gs_solver_free(h)
+            self._h = None
+
+    def set_beta(self, beta):
+        if beta is None:
+            _lib.check(self._lib.gs_solver_set_beta(self._h, None))
+        else:
+            b = np.ascontiguousarray(beta, dtype=np.float64)
+            if b.shape != (self.X.n_cols,):
+                raise ValueError("warm_beta has wrong length")
+            _lib.check(self._lib.gs_solver_set_beta(self._h, _lib.f64p(b)))
+
+    def seq_screen(self, lam: float) -> int:
+        cnt = ctypes.c_int64()
+        _lib.check(self._lib.gs_solver_seq_screen(self._h, float(lam), ctypes.byref(cnt)))
+        return cnt.value
+
+    def solve(self, lam: float, config: SolverConfig, active0=None, active0_mode: int = 0,
+              beta_out: np.ndarray | None = None):
+        """Run solver.py:149-246 on the device; returns (beta, cert, state)."""
+        if config.rule not in _GPU_RULES:
+            raise NotImplementedError(
+                f"rule {config.rule.value!r} is not on the B200 path in this build "
+                f"(supported: none, gap_sphere; SURVEY.md §8(f))")
+        X = self.X
+        n, p = X.n_rows, X.n_cols
+        cap = config.max_passes // config.screen_every + 4
+        beta = np.empty(p) if beta_out is None else beta_out
+        rho = np.empty(n)
+        theta = np.empty(n)
+        active = np.empty(p, dtype=np.int64)
+        tp = np.empty(cap, dtype=np.int64)
+        ta = np.empty(cap, dtype=np.int64)
+        tg = np.empty(cap)
+        tr = np.empty(cap)
+        history = []
+        cb = None
+        user_cb = config.on_checkpoint
+        if config.track_active or user_cb is not None:
+            def _hook(ptr, cnt, _user):
+                a = np.ctypeslib.as_array(ptr, shape=(cnt,)).copy() if cnt else np.empty(0, np.int64)
+                if config.track_active:
+                    history.append(a.copy())
+                if user_cb is not None:
+                    user_cb(a)
+            cb = _lib.CKPT_CB(_hook)
+        cfg = _lib.SolveConfig(float(config.epsilon), int(config.max_passes), int(config.screen_every),
+                               _GPU_RULES[config.rule], int(bool(config.certify)),
+                               cb if cb is not None else _lib.CKPT_CB(), None)
+        res = _lib.SolveResult()
+        res.beta, res.residual, res.theta, res.active = (_lib.f64p(beta), _lib.f64p(rho),
+                                                         _lib.f64p(theta), _lib.i64p(active))
+        res.trace_passes, res.trace_active = _lib.i64p(tp), _lib.i64p(ta)
+        res.trace_gap, res.trace_radius, res.trace_cap = _lib.f64p(tg), _lib.f64p(tr), cap
+        a0 = None
+        n0 = 0
+        if active0_mode == 1:
+            a0 = np.ascontiguousarray(active0, dtype=np.int64)
+            n0 = a0.size
+        _lib.check(self._lib.gs_solver_solve(self._h, float(lam), ctypes.byref(cfg), _lib.i64p(a0), n0,
+                                             int(active0_mode), ctypes.byref(res)))
+        nt = res.n_trace
+        trace = [(int(tp[i]), int(ta[i]), float(tg[i]), float(tr[i])) for i in range(nt)]
+        dual_point = DualPoint(theta=theta, feasibility_margin=float(res.margin),
+                               interpolating=bool(res.interpolating))
+        cert = GapCertificate(primal=float(res.primal), dual=float(res.dual), gap=float(res.gap))
+        state = SolverState(beta=beta, residual=rho, active=active[: res.n_active].copy(),
+                            theta=dual_point, cert=cert, passes_done=int(res.passes_done),
+                            converged=bool(res.converged), screen_trace=trace,
+                            active_history=history)
+        state.stats = dict(cd_visits=int(res.cd_visits), cd_uncertified=int(res.cd_uncertified),
+                           cd_nonzero=int(res.cd_nonzero), checkpoints=int(res.checkpoints),
+                           device_ms=float(res.device_ms))
+        return beta, cert, state
+
+
+def _solver_for(prob: LassoProblem) -> DeviceSolver:
+    s = getattr(prob, "_device_solver", None)
+    if s is None:
+        s = DeviceSolver(prob.X, prob.y)
+        prob._device_solver = s
+    return s
+
+
+def solve(prob: LassoProblem, config: SolverConfig, warm_beta: np.ndarray | None = None,
+          active0: np.ndarray | None = None):
+    """Solve one Lasso problem to duality gap <= config.epsilon (solver.py:149-246).
+
+    Returns (beta, GapCertificate, SolverState); ``state.converged`` is
+    False when the pass budget ran out."""
+    if config.rule not in _GPU_RULES:
+        raise NotImplementedError(
+            f"rule {config.rule.value!r} is not on the B200 path in this build "
+            f"(supported: none, gap_sphere; SURVEY.md §8(f))")
+    if prob.lam > prob.lambda_max * (1 + 1e-12):
+        raise ValueError(f"lambda={prob.lam} exceeds lambda_max={prob.lambda_max}")
+    dev = _solver_for(prob)
+    dev.set_beta(warm_beta)
+    if active0 is None:
+        return dev.solve(prob.lam, config)
+    return dev.solve(prob.lam, config, active0=active0, active0_mode=1)

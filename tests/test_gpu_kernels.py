@@ -1,0 +1,203 @@
+"""Kernel-level parity of the sm_100a kernels against the CPU oracle
+(oracle/kernels.c == reference numba kernels, _kernels.py:14-92).
+
+Exact-order twins must match bit for bit; production kernels (FMA,
+CTA-parallel reductions, certified-zero skipping) within fp64 round-off.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import gapsafe_oracle as O
+
+gs = pytest.importorskip("paper_1505_03410_b200")
+pytestmark = pytest.mark.gpu
+
+
+def _dense(seed, n, p, dtype=np.float64):
+    rng = np.random.default_rng(seed)
+    X = np.asfortranarray(rng.standard_normal((n, p)).astype(dtype))
+    return X, rng
+
+
+def _csc(seed, n, p, density):
+    rng = np.random.default_rng(seed)
+    X = sp.random(n, p, density=density, random_state=np.random.RandomState(seed), format="csc",
+                  data_rvs=lambda k: np.random.RandomState(seed + 1).lognormal(size=k))
+    X.sort_indices()
+    return X, rng
+
+
+@pytest.mark.parametrize("n,p", [(1, 1), (7, 13), (72, 300), (1000, 257), (4096, 40)])
+def test_tdot_exact_order_bitwise(n, p):
+    X, rng = _dense(n * 31 + p, n, p)
+    v = rng.standard_normal(n)
+    cols = rng.permutation(p)[: max(1, p // 2)].astype(np.int64)
+    ref = np.empty(cols.size)
+    O.tdot_dense(X, v, cols, 0.0, ref)
+    D = gs.DesignMatrix(X)
+    out = D.transpose_dot(v, cols, exact_order=True)
+    assert np.array_equal(out, ref)
+
+
+def test_tdot_exact_order_bitwise_f32_storage():
+    X32, rng = _dense(5, 333, 91, np.float32)
+    v = rng.standard_normal(333)
+    cols = np.arange(91, dtype=np.int64)
+    ref = np.empty(91)
+    O.tdot_dense(np.asfortranarray(X32.astype(np.float64)), v, cols, 0.0, ref)
+    out = gs.DesignMatrix(X32).transpose_dot(v, cols, exact_order=True)
+    assert np.array_equal(out, ref)
+
+
+def test_tdot_exact_order_bitwise_csc():
+    X, rng = _csc(3, 500, 400, 0.05)
+    v = rng.standard_normal(500)
+    cols = np.arange(400, dtype=np.int64)[::3].copy()
+    ref = np.empty(cols.size)
+    O.tdot_csc(X.data, X.indices, X.indptr, 500, v, cols, 0.0, ref)
+    out = gs.DesignMatrix(X).transpose_dot(v, cols, exact_order=True)
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("n,p", [(72, 500), (1000, 300), (1, 5), (33, 7)])
+def test_tdot_fast_close(n, p):
+    X, rng = _dense(n + 7 * p, n, p)
+    v = rng.standard_normal(n)
+    D = gs.DesignMatrix(X)
+    full = D.transpose_dot(v)
+    ref = X.T @ v
+    bound = 4 * (n + 2) * 2.0 ** -53 * (np.abs(X).T @ np.abs(v))
+    assert np.all(np.abs(full - ref) <= bound + 1e-300)
+    cols = np.arange(p, dtype=np.int64)[::2].copy()
+    np.testing.assert_array_equal(D.transpose_dot(v, cols), full[cols])
+
+
+@pytest.mark.parametrize("n,p,lam_frac", [(72, 400, 0.3), (1000, 200, 0.1), (20, 50, 0.05),
+                                          (500, 123, 0.5)])
+def test_cd_pass_exact_order_bitwise(n, p, lam_frac):
+    X, rng = _dense(11 * n + p, n, p)
+    y = rng.standard_normal(n)
+    nsq = np.einsum("ij,ij->j", X, X)
+    lam = lam_frac * np.max(np.abs(X.T @ y))
+    active = np.sort(rng.choice(p, size=p * 3 // 4, replace=False)).astype(np.int64)
+    b_ref, r_ref = np.zeros(p), y.copy()
+    b_gpu, r_gpu = np.zeros(p), y.copy()
+    D = gs.DesignMatrix(X)
+    lib = D._lib
+    from paper_1505_03410_b200 import _lib
+    for _ in range(6):
+        O.cd_pass_dense(X, b_ref, r_ref, active, lam, nsq, 0.0)
+        _lib.check(lib.gs_cd_pass(D.handle, _lib.f64p(b_gpu), _lib.f64p(r_gpu), _lib.i64p(active),
+                                  active.size, lam, _lib.f64p(nsq), 0.0, 1))
+        assert np.array_equal(b_gpu, b_ref)
+        assert np.array_equal(r_gpu, r_ref)
+
+
+def test_cd_pass_exact_order_bitwise_csc():
+    X, rng = _csc(9, 400, 300, 0.04)
+    y = rng.standard_normal(400)
+    nsq = np.asarray(X.multiply(X).sum(axis=0)).ravel()
+    keep = np.flatnonzero(nsq > 0).astype(np.int64)
+    lam = 0.2 * np.max(np.abs(X.T @ y))
+    b_ref, r_ref = np.zeros(300), y.copy()
+    b_gpu, r_gpu = np.zeros(300), y.copy()
+    D = gs.DesignMatrix(X)
+    from paper_1505_03410_b200 import _lib
+    for _ in range(5):
+        O.cd_pass_csc(X.data, X.indices, X.indptr, 400, b_ref, r_ref, keep, lam, nsq, 0.0)
+        _lib.check(D._lib.gs_cd_pass(D.handle, _lib.f64p(b_gpu), _lib.f64p(r_gpu), _lib.i64p(keep),
+                                     keep.size, lam, _lib.f64p(nsq), 0.0, 1))
+    assert np.array_equal(b_gpu, b_ref)
+    assert np.array_equal(r_gpu, r_ref)
+
+
+@pytest.mark.parametrize("n,p,lam_frac", [(72, 700, 0.1), (1000, 400, 0.05), (300, 300, 0.02),
+                                          (4000, 60, 0.1), (130, 90, 0.3)])
+def test_cd_pass_production_close(n, p, lam_frac):
+    """Production epoch (certified skipping, CTA reductions) tracks the
+    sequential reference to round-off; supports agree."""
+    X, rng = _dense(3 * n + p, n, p)
+    X /= np.linalg.norm(X, axis=0)
+    X = np.asfortranarray(X)
+    y = rng.standard_normal(n)
+    nsq = np.einsum("ij,ij->j", X, X)
+    lam = lam_frac * np.max(np.abs(X.T @ y))
+    active = np.arange(p, dtype=np.int64)
+    b_ref, r_ref = np.zeros(p), y.copy()
+    D = gs.DesignMatrix(X)
+    st = gs.SolverState(beta=np.zeros(p), residual=y.copy(), active=active, theta=None, cert=None,
+                        passes_done=0, converged=False)
+    prob = gs.LassoProblem(D, y, lam)
+    for _ in range(8):
+        O.cd_pass_dense(X, b_ref, r_ref, active, lam, nsq, 0.0)
+        gs.cd_pass(st, prob)
+    assert np.array_equal(np.flatnonzero(st.beta), np.flatnonzero(b_ref))
+    np.testing.assert_allclose(st.beta, b_ref, rtol=0, atol=1e-11 * max(1, np.abs(b_ref).max()))
+    np.testing.assert_allclose(st.residual, r_ref, rtol=0, atol=1e-11 * np.abs(y).max())
+
+
+def test_cd_pass_production_csc_close():
+    X, rng = _csc(21, 2000, 3000, 0.01)
+    X = sp.csc_matrix(X @ sp.diags(1.0 / np.maximum(np.sqrt(np.asarray(X.multiply(X).sum(0)).ravel()), 1e-300)))
+    y = rng.standard_normal(2000)
+    D = gs.DesignMatrix(X)
+    nsq = np.asarray(X.multiply(X).sum(axis=0)).ravel()
+    active = np.flatnonzero(nsq > 0).astype(np.int64)
+    lam = 0.05 * np.max(np.abs(X.T @ y))
+    b_ref, r_ref = np.zeros(3000), y.copy()
+    st = gs.SolverState(beta=np.zeros(3000), residual=y.copy(), active=active, theta=None, cert=None,
+                        passes_done=0, converged=False)
+    prob = gs.LassoProblem(D, y, lam)
+    for _ in range(5):
+        O.cd_pass_csc(X.data, X.indices, X.indptr, 2000, b_ref, r_ref, active, lam, nsq, 0.0)
+        gs.cd_pass(st, prob)
+    assert np.array_equal(np.flatnonzero(st.beta), np.flatnonzero(b_ref))
+    np.testing.assert_allclose(st.beta, b_ref, rtol=0, atol=1e-11)
+
+
+def test_matvec_axpy_maxcorr():
+    X, rng = _dense(17, 64, 90)
+    D = gs.DesignMatrix(X)
+    beta = np.zeros(90)
+    beta[[3, 17, 40]] = [1.5, -2.0, 0.25]
+    np.testing.assert_allclose(D.matvec(beta), X @ beta, rtol=1e-14, atol=1e-14)
+    v = rng.standard_normal(64)
+    w = v.copy()
+    D.axpy_col(17, 0.7, w)
+    ref = v.copy()
+    ref[:] += 0.7 * X[:, 17]
+    assert np.array_equal(w, ref)                     # elementwise, separate roundings
+    val, j = D.max_abs_correlation(v)
+    c = np.abs(X.T @ v)
+    assert j == int(np.argmax(c)) and val == pytest.approx(c.max(), rel=1e-13)
+    with pytest.raises(IndexError):
+        D.col_dot(90, v)
+    with pytest.raises(ValueError):
+        D.max_abs_correlation(v, restrict=np.array([], dtype=np.int64))
+
+
+def test_max_abs_correlation_tie_smallest_index():
+    D = gs.DesignMatrix(np.eye(3))
+    assert D.max_abs_correlation(np.ones(3))[1] == 0
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_screen_matches_oracle(sparse):
+    rng = np.random.default_rng(8)
+    n, p = 60, 2000
+    if sparse:
+        Xh = sp.random(n, p, density=0.1, random_state=np.random.RandomState(8), format="csc")
+    else:
+        Xh = np.asfortranarray(rng.standard_normal((n, p)))
+    D, Dor = gs.DesignMatrix(Xh), O.DesignMatrix(Xh)
+    c = rng.standard_normal(n) * 0.05
+    for r in (0.0, 0.01, 0.1):
+        a = gs.screen(gs.Sphere(center=c, radius=r), D)
+        b = O.screen(O.Sphere(center=c, radius=r), Dor)
+        # identical masks except features within 1e-10 of the threshold
+        near = np.abs(b.mu - (1 - gs.SCREEN_SAFETY)) <= 1e-10
+        diff = np.setxor1d(a.active_set, b.active_set)
+        assert np.all(near[diff])
+        np.testing.assert_allclose(a.mu, b.mu, rtol=1e-12, atol=1e-14)

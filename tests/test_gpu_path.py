@@ -1,0 +1,186 @@
+"""Path-level parity: solve / run_path on the B200 against the CPU oracle
+(a bit-identical restatement of the reference, tests/test_oracle_golden.py),
+on the same seeded inputs.  See tests/parity.py for the criteria."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import gapsafe_oracle as O
+from paper_1505_03410_b200 import synth
+from parity import compare_paths, compare_states
+
+gs = pytest.importorskip("paper_1505_03410_b200")
+pytestmark = pytest.mark.gpu
+
+
+def _paths(Xh, y, T, delta, eps, rule="gap_sphere", max_passes=100_000, f=10, certify=True):
+    X = gs.DesignMatrix(Xh)
+    dev = gs.DeviceSolver(X, y)
+    Xo = O.DesignMatrix(Xh)
+    lmax, _ = Xo.max_abs_correlation(y)
+    grid = O.lambda_grid(lmax, T, delta)
+    ra = gs.run_path(X, y, grid, gs.SolverConfig(epsilon=eps, max_passes=max_passes, screen_every=f,
+                                                 rule=rule, certify=certify), solver=dev)
+    rb = O.run_path(Xo, y, grid, O.SolverConfig(epsilon=eps, max_passes=max_passes, screen_every=f,
+                                                rule=rule))
+    return ra, rb, float(y @ y)
+
+
+@pytest.mark.parametrize("rule", ["gap_sphere", "none"])
+def test_path_cfg0_shape_small_p(rule):
+    c = synth.cfg0(p=1500)
+    ra, rb, yy = _paths(c.X, c.y, 20, 3.0, c.epsilon, rule=rule)
+    compare_paths(ra, rb, yy)
+
+
+def test_path_cfg0_full():
+    """configs[0] at full size (72 x 7129, 100 lambdas to lambda_max/1e3)."""
+    c = synth.cfg0()
+    ra, rb, yy = _paths(c.X, c.y, c.n_lambdas, c.delta, c.epsilon)
+    compare_paths(ra, rb, yy)
+    assert np.all(ra.converged)
+
+
+def test_path_no_certify_identical_to_certify():
+    """Certified-zero skipping is exact: with and without it the GPU path is
+    bit-identical."""
+    c = synth.cfg0(p=800)
+    X = gs.DesignMatrix(c.X)
+    dev = gs.DeviceSolver(X, c.y)
+    grid = gs.lambda_grid(dev.lambda_max, 15, 2.5)
+    a = gs.run_path(X, c.y, grid, gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000), solver=dev)
+    b = gs.run_path(X, c.y, grid, gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000, certify=False),
+                    solver=dev)
+    assert np.array_equal(a.betas, b.betas)
+    assert [x.gap for x in a.certs] == [x.gap for x in b.certs]
+    assert a.traces == b.traces
+
+
+def test_path_deterministic_bit_identical():
+    """pkg/tests/test_path.py:124-131 on the device."""
+    c = synth.cfg0(p=900)
+    X = gs.DesignMatrix(c.X)
+    grid = gs.lambda_grid(gs.DeviceSolver(X, c.y).lambda_max, 10, 3.0)
+    cfg = gs.SolverConfig(epsilon=1e-8, max_passes=100_000)
+    a = gs.run_path(X, c.y, grid, cfg)
+    b = gs.run_path(X, c.y, grid, cfg)
+    assert np.array_equal(a.betas, b.betas)
+    assert [x.gap for x in a.certs] == [x.gap for x in b.certs]
+
+
+def test_path_cfg1_shape_reduced():
+    """configs[1] generator at reduced width (1000 x 4000)."""
+    c = synth.cfg1(p=4000)
+    ra, rb, yy = _paths(c.X, c.y, 12, 2.0, c.epsilon)
+    compare_paths(ra, rb, yy)
+
+
+def test_path_float32_storage():
+    """fp32 storage / fp64 arithmetic == the oracle on the upcast values."""
+    c = synth.cfg0(p=700)
+    X32 = np.asfortranarray(c.X.astype(np.float32))
+    X64 = np.asfortranarray(X32.astype(np.float64))
+    X = gs.DesignMatrix(X32)
+    Xo = O.DesignMatrix(X64)
+    lmax, _ = Xo.max_abs_correlation(c.y)
+    grid = O.lambda_grid(lmax, 10, 2.0)
+    ra = gs.run_path(X, c.y, grid, gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000))
+    rb = O.run_path(Xo, c.y, grid, O.SolverConfig(epsilon=c.epsilon, max_passes=100_000))
+    compare_paths(ra, rb, float(c.y @ c.y))
+
+
+def test_path_sparse_csc():
+    c = synth.cfg3(p=20_000, n=2_000, nnz_per_col=20)
+    ra, rb, yy = _paths(c.X, c.y, 15, 2.0, c.epsilon)
+    compare_paths(ra, rb, yy)
+
+
+def test_solve_single_lambda_and_hooks():
+    c = synth.cfg0(p=500)
+    X = gs.DesignMatrix(c.X)
+    prob = gs.LassoProblem(X, c.y, 0.1 * gs.DeviceSolver(X, c.y).lambda_max)
+    seen = []
+    cfg = gs.SolverConfig(epsilon=1e-10, max_passes=100_000, track_active=True,
+                          on_checkpoint=lambda a: seen.append(a.size))
+    beta, cert, st = gs.solve(prob, cfg)
+    Xo = O.DesignMatrix(c.X)
+    po = O.LassoProblem(Xo, c.y, prob.lam)
+    b2, c2, st2 = O.solve(po, O.SolverConfig(epsilon=1e-10, max_passes=100_000, track_active=True))
+    compare_states(st, st2, float(c.y @ c.y))
+    assert len(st.active_history) == len(st2.active_history)
+    for a, b in zip(st.active_history, st2.active_history):
+        assert np.array_equal(a, b)
+    assert seen == [a.size for a in st2.active_history]
+
+
+def test_solve_budget_exhausted():
+    c = synth.cfg0(p=300)
+    X = gs.DesignMatrix(c.X)
+    lam = 0.01 * gs.DeviceSolver(X, c.y).lambda_max
+    prob = gs.LassoProblem(X, c.y, lam)
+    beta, cert, st = gs.solve(prob, gs.SolverConfig(epsilon=1e-14, max_passes=3))
+    po = O.LassoProblem(O.DesignMatrix(c.X), c.y, lam)
+    _, _, st2 = O.solve(po, O.SolverConfig(epsilon=1e-14, max_passes=3))
+    assert not st.converged and not st2.converged
+    compare_states(st, st2, float(c.y @ c.y))
+
+
+def test_solve_warm_start_and_active0():
+    c = synth.cfg0(p=400)
+    X = gs.DesignMatrix(c.X)
+    lam = 0.2 * gs.DeviceSolver(X, c.y).lambda_max
+    prob = gs.LassoProblem(X, c.y, lam)
+    b0, _, _ = gs.solve(prob, gs.SolverConfig(epsilon=1e-12, max_passes=100_000))
+    _, _, st = gs.solve(prob, gs.SolverConfig(epsilon=1e-8), warm_beta=b0)
+    assert st.converged and st.passes_done == 0
+    warm = np.ones(400)
+    keep = np.array([0, 3, 7])
+    beta, _, _ = gs.solve(prob, gs.SolverConfig(epsilon=1e-300, max_passes=1), warm_beta=warm,
+                          active0=keep)
+    assert np.all(beta[np.setdiff1d(np.arange(400), keep)] == 0.0)
+
+
+def test_lambda_max_shortcut():
+    c = synth.cfg0(p=300)
+    X = gs.DesignMatrix(c.X)
+    dev = gs.DeviceSolver(X, c.y)
+    prob = gs.LassoProblem(X, c.y, dev.lambda_max)
+    beta, cert, st = gs.solve(prob, gs.SolverConfig())
+    assert np.all(beta == 0) and cert.gap == 0.0 and st.converged and st.passes_done == 0
+    po = O.LassoProblem(O.DesignMatrix(c.X), c.y, prob.lam)
+    _, _, st2 = O.solve(po, O.SolverConfig())
+    assert np.array_equal(st.active, st2.active)
+    assert st.screen_trace == [(0, st2.active.size, 0.0, 0.0)]
+
+
+def test_errors_map_to_reference_exceptions():
+    X = gs.DesignMatrix(np.array([[1.0, 0.0], [0.0, 2.0]]))
+    prob = gs.LassoProblem(X, np.array([1.0, 1.0]), 1.0)
+    th = gs.make_dual_point(X, np.array([5.0, 5.0]))
+    with pytest.raises(gs.InfeasibleDualError):
+        gs.dual_value(prob, th)
+    with pytest.raises(ValueError):
+        gs.LassoProblem(X, np.array([1.0, 1.0]), 2.5)
+    with pytest.raises(gs.NumericalInconsistencyError):
+        gs.gap_radius(prob, -1.0)
+    with pytest.raises(NotImplementedError):
+        gs.solve(prob, gs.SolverConfig(rule="gap_dome"))
+
+
+def test_problem_algebra_hand_values():
+    """pkg/tests/test_problem.py known answers on the 2x2 diagonal problem."""
+    X = gs.DesignMatrix(np.array([[1.0, 0.0], [0.0, 2.0]]))
+    prob = gs.LassoProblem(X, np.array([1.0, 1.0]), 1.0)
+    assert prob.lambda_max == 2.0 and prob.j_star == 1
+    assert gs.primal_value(prob, np.zeros(2)) == 1.0
+    th = gs.make_dual_point(X, np.array([0.5, 0.5]))
+    assert gs.dual_value(prob, th) == pytest.approx(0.75)
+    cert = gs.duality_gap(prob, np.zeros(2), th)
+    assert cert.gap == pytest.approx(0.25)
+    s = gs.region_gap_sphere(prob, np.zeros(2), th)
+    assert s.radius == pytest.approx(np.sqrt(0.5))
+    t = gs.dual_scale(prob, prob.y)
+    np.testing.assert_allclose(t.theta, [0.5, 0.5])
+    assert t.feasibility_margin == pytest.approx(0.0, abs=1e-15)
+    assert gs.dual_scale(prob, np.zeros(2)).interpolating
