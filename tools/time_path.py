@@ -1,0 +1,32 @@
+"""Time one full Lasso path on the GPU (and optionally the oracle) for a config."""
+import sys, time, json, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_1505_03410_b200 as gs
+from paper_1505_03410_b200 import synth
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg0"
+kw = {}
+if len(sys.argv) > 2:
+    kw["p"] = int(sys.argv[2])
+c = synth.by_name(name, **kw)
+t0 = time.perf_counter()
+X = gs.DesignMatrix(c.X)
+dev = gs.DeviceSolver(X, c.y)
+grid = gs.lambda_grid(dev.lambda_max, c.n_lambdas, c.delta)
+cfg = gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000)
+t1 = time.perf_counter()
+res = gs.run_path(X, c.y, grid, cfg, solver=dev)
+t2 = time.perf_counter()
+res = gs.run_path(X, c.y, grid, cfg, solver=dev)
+t3 = time.perf_counter()
+st = [s.stats for s in res.states]
+out = dict(config=name, upload_s=t1 - t0, path_s_first=t2 - t1, path_s=t3 - t2,
+           epochs=int(sum(s.passes_done for s in res.states)),
+           checkpoints=int(sum(x["checkpoints"] for x in st)),
+           cd_visits=int(sum(x["cd_visits"] for x in st)),
+           cd_uncertified=int(sum(x["cd_uncertified"] for x in st)),
+           cd_nonzero=int(sum(x["cd_nonzero"] for x in st)),
+           device_ms=float(sum(x["device_ms"] for x in st)),
+           converged=int(res.converged.sum()))
+print(json.dumps(out))
