@@ -1,0 +1,277 @@
+"""Benchmark: Lasso-path wall time to gap 1e-8 (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+
+A "step" is one full warm-started Gap Safe Lasso path over the config's
+lambda grid.  ``value`` is the path wall time measured on
+the device with CUDA events bracketing the path on the solver's stream
+(inputs resident in HBM); ``e2e`` is the same path through the public API
+from pinned host buffers (design + response H2D, coefficients D2H inside the
+timed region).  At N > 1 every rank runs an independent replica of the path
+(cfg1 does not shard: "replicas only"); the reported time is the
+max over ranks.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port of /root/reference/pkg/src/gapsafe, bit-identical to it, see
+tests/test_oracle_golden.py) on a bounded sample of the same workload: the
+first lambdas of the same path, as many as fit the time budget.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Lasso-path wall time to gap 1e-8 (s); screening-pass HBM GB/s vs peak"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _make_case(name):
+    from paper_1505_03410_b200 import synth
+    return synth.by_name(name)
+
+
+def _grid(lmax, case):
+    from paper_1505_03410_b200 import lambda_grid
+    return lambda_grid(lmax, case.n_lambdas, case.delta)
+
+
+def _cpu_sample(case, grid, budget_s):
+    """Oracle (reference algorithm, CPU) on the first lambdas of the same path,
+    stopping after the point at which the budget is exceeded."""
+    from oracle import gapsafe_oracle as O
+    X = O.DesignMatrix(case.X)
+    t0 = time.perf_counter()
+    res = O.run_path(X, case.y, grid, O.SolverConfig(epsilon=case.epsilon, max_passes=100_000),
+                     cache_lambda_max=True, time_budget_s=budget_s)
+    wall = time.perf_counter() - t0
+    return res, wall
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    case = _make_case(args.config)
+    from oracle import gapsafe_oracle as O
+    Xo = O.DesignMatrix(case.X)
+    lmax, _ = Xo.max_abs_correlation(case.y)
+    grid = O.lambda_grid(lmax, case.n_lambdas, case.delta)
+    cores = len(os.sched_getaffinity(0))
+    times, npts = [], None
+    for step in range(args.warmup + args.steps):
+        res, wall = _cpu_sample(case, grid if npts is None else grid[:npts], args.cpu_budget)
+        if npts is None:
+            npts = len(res.timings)
+        if step >= args.warmup:
+            times.append(sum(res.timings))
+    value = statistics.median(times)
+    sample = f"first {npts} of {grid.size} lambdas of the {args.config} path (run_path timing scope, path.py:78,94)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, SURVEY.md §8(d))",
+            "config": {"workload": args.config, "n": int(case.X.shape[0]), "p": int(case.X.shape[1]),
+                       "lambdas": int(grid.size), "sample_lambdas": npts, "tol": case.tol},
+            "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    ws, rank, local = _dist()
+    import paper_1505_03410_b200 as gs
+    from paper_1505_03410_b200 import _lib
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    _lib.init_device(local)
+    case = _make_case(args.config)
+    n, p = case.X.shape
+    X = gs.DesignMatrix(case.X)
+    dev = gs.DeviceSolver(X, case.y)
+    grid = _grid(dev.lambda_max, case)
+    cfg = gs.SolverConfig(epsilon=case.epsilon, max_passes=100_000)
+    timer = gs.PathTimer(dev)
+
+    def one_path():
+        timer.start()
+        res = gs.run_path(X, case.y, grid, cfg, solver=dev)
+        return res, timer.stop_ms()
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        one_path()
+    barrier()
+    l0 = _lib.launch_count()
+    ms, results = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            res, t = one_path()
+            ms.append(t)
+            results.append(res)
+    launches = (_lib.launch_count() - l0) / args.steps
+    barrier()
+    ms_step = statistics.mean(ms)
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        tt = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+    res = results[-1]
+    st = [s.stats for s in res.states]
+    agg = {k: sum(x[k] for x in st) for k in ("cd_visits", "cd_uncertified", "cd_nonzero", "checkpoints",
+                                             "screen_ms", "ckpt_ms", "refresh_ms", "cd_ms", "n_screen",
+                                             "n_refresh")}
+    epochs = int(sum(s.passes_done for s in res.states))
+
+    # ---- screening-pass roofline: the fused full-p GEMV + sphere test + compaction
+    peak, peak_kind = _peaks()
+    es = 8 if case.X.dtype == np.float64 else 4
+    scr_bytes = n * p * es + p * (8 + 4) + n * 8       # X, norms + indices out, center
+    scr_ms = timer.screen_pass_ms(X, res.states[-1].theta.theta, 1e-3, reps=10)
+    achieved = scr_bytes / (scr_ms * 1e-3) / 1e9
+    inpath_screen = agg["screen_ms"] / max(1, agg["n_screen"])
+
+    # ---- e2e through the public API from pinned host buffers
+    e2e_ms, h2d, d2h = timer.e2e_path_ms(case, grid, cfg, reps=max(1, min(args.steps, 2)))
+
+    line = {
+        "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md §8(d))",
+        "config": {"workload": args.config, "n": int(n), "p": int(p), "lambdas": int(grid.size),
+                   "tol": case.tol, "screen_every": 10, "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": f"design {n * p * es / 1e6:.0f} MB > 126 MB L2: streamed inputs, no flush needed"},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "group_gemv/k_gemv_t_dense G_MU (full-p sequential screen)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "bytes_per_launch": scr_bytes, "launch_ms": scr_ms,
+                     "in_path_screen_ms": inpath_screen},
+        "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "path": {"epochs": epochs, "checkpoints": agg["checkpoints"], "converged": int(res.converged.sum()),
+                 "cd_visits": agg["cd_visits"], "cd_uncertified": agg["cd_uncertified"],
+                 "cd_nonzero": agg["cd_nonzero"], "refreshes": agg["n_refresh"],
+                 "phase_ms": {"screen": agg["screen_ms"], "checkpoint": agg["ckpt_ms"],
+                              "refresh": agg["refresh_ms"], "cd": agg["cd_ms"]},
+                 "cd_updates_per_s": agg["cd_uncertified"] / max(1e-9, agg["cd_ms"] * 1e-3)},
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        sample, wall = _cpu_sample(case, grid, args.cpu_budget)
+        k = len(sample.timings)
+        gpu_same = sum(res.timings[:k])
+        line["cpu_baseline"] = {"value": sum(sample.timings), "unit": "s", "cores": len(os.sched_getaffinity(0)),
+                                "kind": "port",
+                                "sample": f"first {k} of {grid.size} lambdas of the {args.config} path",
+                                "gpu_same_sample_s": gpu_same,
+                                "speedup_same_sample": sum(sample.timings) / max(gpu_same, 1e-12)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -47,6 +47,8 @@ int gs_init(int device);
 int gs_device_count(int *count);
 const char *gs_last_error(void);
 const char *gs_version(void);
+/* number of kernels this library has launched so far in this process */
+int64_t gs_launch_count(void);
 
 /* ---- DesignMatrix storage (design_matrix.py:34-57) ----------------------- */
 /* Dense column-major design, column j at X + j*ld_host (F-order numpy array).
@@ -123,6 +125,9 @@ typedef struct {
     uint64_t cd_visits, cd_uncertified, cd_nonzero;
     int64_t checkpoints;
     double device_ms;
+    /* in-kernel phase times (device %globaltimer, ms) and counts */
+    double screen_ms, ckpt_ms, refresh_ms, cd_ms;
+    int64_t n_screen, n_refresh, launches;
 } gs_solve_result;
 
 /* y is uploaded once; lambda_max = |X^T y|_inf is computed once and cached
@@ -139,6 +144,19 @@ int gs_solver_seq_screen(gs_solver *S, double lam, int64_t *n_active);
 int gs_solver_solve(gs_solver *S, double lam, const gs_solve_config *cfg, const int64_t *active0,
                     int64_t n0, int active0_mode, gs_solve_result *res);
 void gs_solver_free(gs_solver *S);
+
+/* ---- measurement support ---------------------------------------------------- */
+/* CUDA events on the solver's stream: op 0 records the start, op 1 records the
+ * stop, synchronizes and returns the elapsed milliseconds in *ms. */
+int gs_solver_timer(gs_solver *S, int op, double *ms);
+/* The full-p sphere screening pass (fused GEMV + test, then stable compaction)
+ * launched `reps` times on the matrix stream, timed with CUDA events; *ms is the
+ * average per pass, *n_active the survivors of the last pass. */
+int gs_screen_timed(const gs_matrix *M, const double *center, double radius, int reps, double *ms,
+                    int64_t *n_active);
+/* pinned (page-locked) host memory for H2D/D2H at full PCIe rate */
+int gs_host_alloc(int64_t bytes, void **out);
+void gs_host_free(void *ptr);
 
 #ifdef __cplusplus
 }

@@ -483,12 +483,14 @@ class PathResult:
     states: list = field(default_factory=list)
 
 
-def run_path(X, y, grid, config, cache_lambda_max=False, max_points=None):
+def run_path(X, y, grid, config, cache_lambda_max=False, max_points=None, time_budget_s=None):
     """path.py:52-105.
 
     ``cache_lambda_max`` skips the identical per-lambda X^T y pass
-    (problem.py:50); ``max_points`` stops after that many grid points (the
-    bounded CPU-baseline sample).  Both default to the reference behaviour.
+    (problem.py:50); ``max_points`` stops after that many grid points and
+    ``time_budget_s`` after the point at which the cumulative per-lambda time
+    exceeds the budget (the bounded CPU-baseline sample).  The defaults give
+    the reference behaviour.
     """
     grid = np.asarray(grid, dtype=np.float64)
     if grid.size == 0:
@@ -521,5 +523,8 @@ def run_path(X, y, grid, config, cache_lambda_max=False, max_points=None):
         states.append(state)
         conv[t] = state.converged
         prev_beta, prev_theta, prev_resid = beta, state.theta, state.residual
-    return PathResult(lambdas=grid[:T], betas=betas, certs=certs, traces=traces,
-                      timings=timings, converged=conv, states=states)
+        if time_budget_s is not None and sum(timings) >= time_budget_s:
+            T = t + 1
+            break
+    return PathResult(lambdas=grid[:T], betas=betas[:T], certs=certs, traces=traces,
+                      timings=timings, converged=conv[:T], states=states)

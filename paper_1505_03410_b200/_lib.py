@@ -54,7 +54,9 @@ class SolveResult(ctypes.Structure):
                 ("pad_", c_i32),
                 ("margin", c_dbl), ("primal", c_dbl), ("dual", c_dbl), ("gap", c_dbl),
                 ("cd_visits", ctypes.c_uint64), ("cd_uncertified", ctypes.c_uint64),
-                ("cd_nonzero", ctypes.c_uint64), ("checkpoints", c_i64), ("device_ms", c_dbl)]
+                ("cd_nonzero", ctypes.c_uint64), ("checkpoints", c_i64), ("device_ms", c_dbl),
+                ("screen_ms", c_dbl), ("ckpt_ms", c_dbl), ("refresh_ms", c_dbl), ("cd_ms", c_dbl),
+                ("n_screen", c_i64), ("n_refresh", c_i64), ("launches", c_i64)]
 
 
 # every symbol declared in include/gapsafe_b200.h with its ctypes signature
@@ -63,6 +65,7 @@ SIGNATURES = {
     "gs_device_count": (c_i32, [ctypes.POINTER(ctypes.c_int)]),
     "gs_last_error": (ctypes.c_char_p, []),
     "gs_version": (ctypes.c_char_p, []),
+    "gs_launch_count": (c_i64, []),
     "gs_matrix_dense": (c_i32, [c_vp, ctypes.c_int, c_i64, c_i64, c_i64, P_f64, ctypes.POINTER(c_vp)]),
     "gs_matrix_csc": (c_i32, [P_f64, P_i32, P_i64, c_i64, c_i64, P_f64, ctypes.POINTER(c_vp)]),
     "gs_matrix_norms_sq": (c_i32, [c_vp, P_f64]),
@@ -82,6 +85,10 @@ SIGNATURES = {
     "gs_solver_solve": (c_i32, [c_vp, c_dbl, ctypes.POINTER(SolveConfig), P_i64, c_i64,
                                 ctypes.c_int, ctypes.POINTER(SolveResult)]),
     "gs_solver_free": (None, [c_vp]),
+    "gs_solver_timer": (c_i32, [c_vp, ctypes.c_int, P_f64]),
+    "gs_screen_timed": (c_i32, [c_vp, P_f64, c_dbl, ctypes.c_int, P_f64, P_i64]),
+    "gs_host_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
+    "gs_host_free": (None, [c_vp]),
 }
 
 _lib = None
@@ -140,6 +147,16 @@ def i32p(a: np.ndarray | None):
     return None if a is None else a.ctypes.data_as(P_i32)
 
 
+def launch_count() -> int:
+    """Kernels launched by libgapsafe_b200 in this process so far."""
+    return int(load().gs_launch_count())
+
+
+def init_device(index: int) -> None:
+    """Bind the library to CUDA device ``index`` (one process per GPU)."""
+    check(load().gs_init(int(index)))
+
+
 def vec_stats(a: np.ndarray, b: np.ndarray | None = None) -> tuple[float, float]:
     """(a.b, sum|a|) reduced on the device."""
     a = np.ascontiguousarray(a, dtype=np.float64)
@@ -149,3 +166,20 @@ def vec_stats(a: np.ndarray, b: np.ndarray | None = None) -> tuple[float, float]
     asum = c_dbl()
     check(load().gs_vec_stats(f64p(a), f64p(b), a.size, ctypes.byref(dot), ctypes.byref(asum)))
     return dot.value, asum.value
+
+
+class PinnedArray:
+    """A numpy view of page-locked host memory (freed with the object)."""
+
+    def __init__(self, shape, dtype=np.float64, order="C"):
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        ptr = c_vp()
+        check(load().gs_host_alloc(self.nbytes, ctypes.byref(ptr)))
+        self._ptr = ptr
+        buf = (ctypes.c_char * self.nbytes).from_address(ptr.value)
+        self.array = np.ndarray(shape, dtype=dtype, buffer=buf, order=order)
+
+    def __del__(self):
+        if getattr(self, "_ptr", None) is not None and self._ptr.value:
+            load().gs_host_free(self._ptr)
+            self._ptr = None

@@ -3,7 +3,11 @@
 // (solver.py:149-246, path.py:82-91), all behind the C ABI of
 // include/gapsafe_b200.h.
 #include "../../include/gapsafe_b200.h"
-#include "gs_kernels.cuh"
+#include "gs_solve.cuh"
+
+#include <cmath>
+#include <cstdlib>
+#include <cstddef>
 
 #include <algorithm>
 #include <cstdio>
@@ -44,6 +48,8 @@ static int fail(int code, const std::string& msg) {
     } while (0)
 
 static int g_device = -1;
+static int64_t g_launches = 0;   // kernels launched by this library (bench evidence)
+#define COUNT_LAUNCH(k) (g_launches += (k))
 
 static int ensure_device() {
     if (g_device >= 0) return GS_OK;
@@ -141,6 +147,7 @@ extern "C" int gs_device_count(int* count) {
 
 extern "C" const char* gs_last_error(void) { return g_err.c_str(); }
 extern "C" const char* gs_version(void) { return "gapsafe_b200 0.1.0 (sm_100a)"; }
+extern "C" int64_t gs_launch_count(void) { return g_launches; }
 
 extern "C" int gs_matrix_dense(const void* X, int dtype, int64_t n, int64_t p, int64_t ld_host,
                                const double* norms_sq, gs_matrix** out) {
@@ -251,6 +258,7 @@ static int launch_gemv(const gs_matrix* M, cudaStream_t st, GemvArgs a, int64_t*
     a.cpb = gemv_cpb(a.m);
     const int64_t nb = (a.m + a.cpb - 1) / a.cpb;
     if (nblocks_out) *nblocks_out = nb;
+    COUNT_LAUNCH(1);
     if (M->sparse) {
         k_gemv_t_csc<<<(unsigned)nb, 256, 0, st>>>(M->data, M->indices, M->indptr, a);
     } else {
@@ -275,6 +283,7 @@ static int launch_compact(cudaStream_t st, Scratch& s, const uint8_t* flags, int
         CK(cudaMemsetAsync(count_dev, 0, sizeof(int64_t), st));
         return GS_OK;
     }
+    COUNT_LAUNCH(3);
     k_compact_count<<<(unsigned)nb, 256, 0, st>>>(flags, m, s.cnt);
     k_scan_counts<<<1, 1024, 0, st>>>(s.cnt, nb, s.off, count_dev);
     k_compact_scatter<<<(unsigned)nb, 256, 0, st>>>(flags, m, cols, s.off, out);
@@ -465,32 +474,96 @@ extern "C" int gs_vec_stats(const double* a, const double* b, int64_t n, double*
     return GS_OK;
 }
 
-// CD epoch launch: (block, rows-per-thread) from n.
-template <typename T>
-static int launch_cd_dense(const gs_matrix* M, cudaStream_t st, const CdArgs& a) {
-    const int64_t n = M->n;
-    const T* X = (const T*)M->X;
-    if (n <= 128) k_cd_epoch_dense<T, 1><<<1, 128, 0, st>>>(X, a);
-    else if (n <= 256) k_cd_epoch_dense<T, 1><<<1, 256, 0, st>>>(X, a);
-    else if (n <= 512) k_cd_epoch_dense<T, 2><<<1, 256, 0, st>>>(X, a);
-    else if (n <= 1024) k_cd_epoch_dense<T, 4><<<1, 256, 0, st>>>(X, a);
-    else if (n <= 2048) k_cd_epoch_dense<T, 8><<<1, 256, 0, st>>>(X, a);
-    else if (n <= 4096) k_cd_epoch_dense<T, 8><<<1, 512, 0, st>>>(X, a);
-    else return fail(GS_ERR_VALUE, "dense CD kernel supports n <= 4096 in this build");
+// ---------------------------------------------------------------------------
+// persistent solve: launch configuration
+// ---------------------------------------------------------------------------
+constexpr int kSolveThreads = 256;
+
+struct CdShape { int R, W; };
+
+static CdShape cd_shape(int64_t n) {
+    // rows per lane R (template) and CD warp-group size W: W*32*R >= n
+    if (n <= 32) return {1, 1};
+    if (n <= 64) return {2, 1};
+    if (n <= 128) return {4, 1};
+    if (n <= 256) return {8, 1};
+    if (n <= 1024) return {4, (int)((n + 127) / 128)};
+    if (n <= 2048) return {8, (int)((n + 255) / 256)};
+    return {0, 0};
+}
+
+template <typename T, int R>
+static int launch_solve_T(cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem) {
+    auto kern = k_solve<T, R>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int G_ = G;
+    void* args[] = {(void*)&dprobs, (void*)&G_};
+    COUNT_LAUNCH(1);
+    CK(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)(G * nprob)), dim3(kSolveThreads), args, smem, st));
+    return GS_OK;
+}
+
+static int launch_solve(const gs_matrix* M, cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem,
+                        int R) {
+    if (M->sparse || M->dtype == GS_DTYPE_F64) {
+        switch (R) {
+            case 1: return launch_solve_T<double, 1>(st, dprobs, G, nprob, smem);
+            case 2: return launch_solve_T<double, 2>(st, dprobs, G, nprob, smem);
+            case 4: return launch_solve_T<double, 4>(st, dprobs, G, nprob, smem);
+            default: return launch_solve_T<double, 8>(st, dprobs, G, nprob, smem);
+        }
+    }
+    switch (R) {
+        case 1: return launch_solve_T<float, 1>(st, dprobs, G, nprob, smem);
+        case 2: return launch_solve_T<float, 2>(st, dprobs, G, nprob, smem);
+        case 4: return launch_solve_T<float, 4>(st, dprobs, G, nprob, smem);
+        default: return launch_solve_T<float, 8>(st, dprobs, G, nprob, smem);
+    }
+}
+
+template <typename T, int R>
+static int launch_cdpass_T(cudaStream_t st, const SolveDev* dprobs, size_t smem) {
+    auto kern = k_cd_pass_prod<T, R>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    COUNT_LAUNCH(1);
+    kern<<<1, kSolveThreads, smem, st>>>(dprobs);
     CKL();
     return GS_OK;
 }
 
-static int launch_cd(const gs_matrix* M, cudaStream_t st, const CdArgs& a) {
+static int launch_cdpass(const gs_matrix* M, cudaStream_t st, const SolveDev* dprobs, size_t smem, int R) {
+    if (M->sparse || M->dtype == GS_DTYPE_F64) {
+        switch (R) {
+            case 1: return launch_cdpass_T<double, 1>(st, dprobs, smem);
+            case 2: return launch_cdpass_T<double, 2>(st, dprobs, smem);
+            case 4: return launch_cdpass_T<double, 4>(st, dprobs, smem);
+            default: return launch_cdpass_T<double, 8>(st, dprobs, smem);
+        }
+    }
+    switch (R) {
+        case 1: return launch_cdpass_T<float, 1>(st, dprobs, smem);
+        case 2: return launch_cdpass_T<float, 2>(st, dprobs, smem);
+        case 4: return launch_cdpass_T<float, 4>(st, dprobs, smem);
+        default: return launch_cdpass_T<float, 8>(st, dprobs, smem);
+    }
+}
+
+static int vs_cap_for(const gs_matrix* M) { return M->sparse ? 24576 : 6144; }
+
+static size_t solve_smem(const gs_matrix* M) {
+    const int64_t n = M->n;
+    const size_t vs = (n <= vs_cap_for(M)) ? (size_t)(n + 2) * 8 : 0;
+    if (M->sparse) return std::max(vs, (size_t)kTTile * sizeof(float) + (size_t)n * 8);
+    return (size_t)kCdBytes + vs;     // dense: CD tile stays resident beside the GEMV staging
+}
+
+static int check_shape(const gs_matrix* M) {
     if (M->sparse) {
-        const size_t sm = (size_t)M->n * 8;
-        if (sm > 200 * 1024) return fail(GS_ERR_VALUE, "sparse CD kernel supports n <= 25600 in this build");
-        if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_cd_epoch_csc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_cd_epoch_csc<<<1, 1024, sm, st>>>(M->data, M->indices, M->indptr, a);
-        CKL();
+        if (solve_smem(M) > 220 * 1024) return fail(GS_ERR_VALUE, "sparse solver supports n <= 24576 in this build");
         return GS_OK;
     }
-    return M->dtype == GS_DTYPE_F64 ? launch_cd_dense<double>(M, st, a) : launch_cd_dense<float>(M, st, a);
+    if (cd_shape(M->n).R == 0) return fail(GS_ERR_VALUE, "dense solver supports n <= 2048 in this build");
+    return GS_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -500,34 +573,49 @@ struct gs_solver {
     const gs_matrix* M = nullptr;
     cudaStream_t st = nullptr;
     int64_t n = 0, p = 0;
-    double *y = nullptr, *beta = nullptr, *rho = nullptr, *theta = nullptr, *c = nullptr, *t = nullptr;
+    double *y = nullptr, *beta = nullptr, *rho = nullptr, *theta = nullptr, *c = nullptr;
+    float *t = nullptr, *t2 = nullptr;
     int32_t *A = nullptr, *A2 = nullptr, *S = nullptr, *Dl = nullptr;
-    uint8_t *flags = nullptr, *flags2 = nullptr, *mark = nullptr;
+    uint8_t *flags = nullptr, *mark = nullptr;
     double* partial = nullptr;
     int nch_max = 0;
     Scratch s;
     DevScalars* sc = nullptr;     // device
     DevScalars* hs = nullptr;     // pinned host mirror
+    SolveCtl* ctl = nullptr;
+    SolveCtl* hctl = nullptr;
+    GroupBar* bar = nullptr;
+    double* cta_val = nullptr;
+    int64_t* cta_idx = nullptr;
+    int64_t* cta_cnt = nullptr;
+    SolveDev* dprob = nullptr;
     TraceRow* trace = nullptr;
     int64_t trace_cap = 0;
+    int G = 1;
     double lmax = 0.0, y_norm_sq = 0.0;
     int64_t jstar = 0;
-    int64_t m = 0;                // current active count (host mirror)
-    bool has_prev = false;
+    int64_t m = 0;                // active count after the last solve
+    bool has_prev = false, seq_pending = false;
+    double seq_lam = 0.0;
     double prev_margin = 1.0;
     int prev_interp = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t tev0 = nullptr, tev1 = nullptr;   // gs_solver_timer (bench)
 };
 
 static void solver_release(gs_solver* S) {
     if (!S) return;
-    cudaFree(S->y); cudaFree(S->beta); cudaFree(S->rho); cudaFree(S->theta); cudaFree(S->c); cudaFree(S->t);
+    cudaFree(S->y); cudaFree(S->beta); cudaFree(S->rho); cudaFree(S->theta); cudaFree(S->c);
+    cudaFree(S->t); cudaFree(S->t2);
     cudaFree(S->A); cudaFree(S->A2); cudaFree(S->S); cudaFree(S->Dl);
-    cudaFree(S->flags); cudaFree(S->flags2); cudaFree(S->mark); cudaFree(S->partial);
-    cudaFree(S->sc); cudaFreeHost(S->hs); cudaFree(S->trace);
+    cudaFree(S->flags); cudaFree(S->mark); cudaFree(S->partial);
+    cudaFree(S->sc); cudaFreeHost(S->hs); cudaFree(S->ctl); cudaFreeHost(S->hctl); cudaFree(S->bar);
+    cudaFree(S->cta_val); cudaFree(S->cta_idx); cudaFree(S->cta_cnt); cudaFree(S->dprob); cudaFree(S->trace);
     S->s.release();
     if (S->ev0) cudaEventDestroy(S->ev0);
     if (S->ev1) cudaEventDestroy(S->ev1);
+    if (S->tev0) cudaEventDestroy(S->tev0);
+    if (S->tev1) cudaEventDestroy(S->tev1);
     if (S->st) cudaStreamDestroy(S->st);
     delete S;
 }
@@ -538,31 +626,55 @@ static int sc_upload(gs_solver* S) {
 }
 static int sc_download(gs_solver* S) {
     CK(cudaMemcpyAsync(S->hs, S->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, S->st));
+    CK(cudaMemcpyAsync(S->hctl, S->ctl, sizeof(SolveCtl), cudaMemcpyDeviceToHost, S->st));
     CK(cudaStreamSynchronize(S->st));
     return GS_OK;
 }
 
+// CTAs cooperating on one problem: enough to stream the design at HBM rate,
+// few enough that the group barrier stays cheap for small problems.
+static int choose_group(const gs_matrix* M) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* env = getenv("GS_GROUP_CTAS");
+    if (env && atoi(env) > 0) return std::min(atoi(env), sms);
+    const double bytes = M->sparse ? (double)M->nnz * 12.0 : (double)M->ld * M->p * (M->dtype == GS_DTYPE_F64 ? 8 : 4);
+    const int g = (int)std::ceil(bytes / (1 << 20));
+    return std::max(1, std::min(sms, g));
+}
+
 extern "C" int gs_solver_create(const gs_matrix* M, const double* y, gs_solver** out) {
     TRY(ensure_device());
+    TRY(check_shape(M));
     gs_solver* S = new gs_solver();
     S->M = M; S->n = M->n; S->p = M->p;
     int rc = [&]() -> int {
         const int64_t n = S->n, p = S->p;
+        S->G = choose_group(M);
         CK(cudaStreamCreateWithFlags(&S->st, cudaStreamNonBlocking));
         CK(cudaEventCreate(&S->ev0)); CK(cudaEventCreate(&S->ev1));
+        CK(cudaEventCreate(&S->tev0)); CK(cudaEventCreate(&S->tev1));
         TRY(dalloc(&S->y, n + 2)); TRY(dalloc(&S->rho, n + 2)); TRY(dalloc(&S->theta, n + 2));
-        TRY(dalloc(&S->beta, p)); TRY(dalloc(&S->c, p)); TRY(dalloc(&S->t, p));
+        TRY(dalloc(&S->beta, p)); TRY(dalloc(&S->c, p)); TRY(dalloc(&S->t, p)); TRY(dalloc(&S->t2, p));
         TRY(dalloc(&S->A, p)); TRY(dalloc(&S->A2, p)); TRY(dalloc(&S->S, p)); TRY(dalloc(&S->Dl, p));
-        TRY(dalloc(&S->flags, p)); TRY(dalloc(&S->flags2, p)); TRY(dalloc(&S->mark, p));
-        S->nch_max = (int)std::min<int64_t>(256, std::max<int64_t>(1, (p + 31) / 32));
+        TRY(dalloc(&S->flags, p)); TRY(dalloc(&S->mark, p));
+        S->nch_max = (int)std::min<int64_t>(256, std::max<int64_t>(1, (p + 15) / 16));
         if (!M->sparse) TRY(dalloc(&S->partial, (size_t)S->nch_max * n));
         TRY(S->s.alloc(p));
-        TRY(dalloc(&S->sc, 1));
+        TRY(dalloc(&S->sc, 1)); TRY(dalloc(&S->ctl, 1)); TRY(dalloc(&S->bar, 1));
+        TRY(dalloc(&S->cta_val, S->G)); TRY(dalloc(&S->cta_idx, S->G)); TRY(dalloc(&S->cta_cnt, 2 * S->G));
+        TRY(dalloc(&S->dprob, 1));
         CK(cudaMallocHost((void**)&S->hs, sizeof(DevScalars)));
+        CK(cudaMallocHost((void**)&S->hctl, sizeof(SolveCtl)));
         memset(S->hs, 0, sizeof(DevScalars));
+        memset(S->hctl, 0, sizeof(SolveCtl));
+        CK(cudaMemsetAsync(S->bar, 0, sizeof(GroupBar), S->st));
         CK(cudaMemsetAsync(S->mark, 0, p, S->st));
         CK(cudaMemsetAsync(S->beta, 0, p * 8, S->st));
         CK(cudaMemsetAsync(S->y, 0, (n + 2) * 8, S->st));
+        CK(cudaMemsetAsync(S->rho, 0, (n + 2) * 8, S->st));
+        CK(cudaMemsetAsync(S->theta, 0, (n + 2) * 8, S->st));
         CK(cudaMemcpyAsync(S->y, y, n * 8, cudaMemcpyHostToDevice, S->st));
         TRY(sc_upload(S));
         // lambda_max = |X^T y|_inf, j_star (problem.py:50), ||y||^2 (problem.py:54)
@@ -606,127 +718,43 @@ extern "C" int gs_solver_set_beta(gs_solver* S, const double* beta) {
 
 extern "C" void gs_solver_free(gs_solver* S) { solver_release(S); }
 
-static int status_error(int32_t st, const DevScalars* h, bool seq) {
+static int status_error(int32_t st, double margin, double gap) {
     char buf[256];
     if (st == ST_INFEASIBLE) {
-        snprintf(buf, sizeof buf, "dual point infeasible: margin=%.17g", seq ? h->margin : h->margin);
+        snprintf(buf, sizeof buf, "dual point infeasible: margin=%.17g", margin);
         return fail(GS_ERR_INFEASIBLE, buf);
     }
     if (st == ST_NEG_GAP) {
-        snprintf(buf, sizeof buf, "negative duality gap beyond tolerance: %.17g", h->gap_pre);
+        snprintf(buf, sizeof buf, "negative duality gap beyond tolerance: %.17g", gap);
         return fail(GS_ERR_NUMERICAL, buf);
     }
     return GS_OK;
 }
 
-// rho = y - X beta over the current support (beta is zero off A)
-static int resync(gs_solver* S) {
-    const gs_matrix* M = S->M;
-    cudaStream_t st = S->st;
-    const int n = (int)S->n;
-    if (M->sparse) {
-        k_resync_csr<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(M->csr_data, M->csr_cols, M->csr_rowptr, n, S->beta, S->y, S->rho);
-        CKL();
-        return GS_OK;
-    }
-    const int64_t m = S->m;
-    k_flags_beta_nz<<<grid_for(std::max<int64_t>(m, 1), 256), 256, 0, st>>>(S->A, m, S->beta, S->flags);
-    CKL();
-    TRY(launch_compact(st, S->s, S->flags, m, S->A, S->S, &S->sc->n_supp));
-    const int nch = (int)std::min<int64_t>(S->nch_max, std::max<int64_t>(1, (m + 31) / 32));
-    dim3 g((unsigned)((n + 255) / 256), (unsigned)nch);
-    if (M->dtype == GS_DTYPE_F64)
-        k_resync_partial_dense<double><<<g, 256, 0, st>>>((const double*)M->X, M->ld, n, S->S, &S->sc->n_supp, S->beta, nch, S->partial);
-    else
-        k_resync_partial_dense<float><<<g, 256, 0, st>>>((const float*)M->X, M->ld, n, S->S, &S->sc->n_supp, S->beta, nch, S->partial);
-    k_resync_final<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(S->y, S->partial, nch, n, S->rho);
-    CKL();
-    return GS_OK;
-}
-
-// restricted (A) or unrestricted (all p) |X^T rho|_inf into sc->corr; dots into c.
-static int dual_corr(gs_solver* S, bool restricted) {
-    GemvArgs a{};
-    a.v = S->rho; a.cols = restricted ? S->A : nullptr; a.m = restricted ? S->m : S->p;
-    a.mode = GEMV_MAX; a.out_c = restricted ? S->c : nullptr;
-    a.blk_val = S->s.blk_val; a.blk_idx = S->s.blk_idx;
-    int64_t nb = 0;
-    TRY(launch_gemv(S->M, S->st, a, &nb));
-    k_max_finalize<<<1, 1024, 0, S->st>>>(S->s.blk_val, S->s.blk_idx, nb, &S->sc->corr, &S->sc->corr_arg);
-    CKL();
-    return GS_OK;
-}
-
-static int cd_epoch(gs_solver* S, bool certify) {
-    const gs_matrix* M = S->M;
-    if (S->m == 0) return GS_OK;
-    if (certify) {
-        GemvArgs a{};
-        a.v = S->rho; a.cols = S->A; a.m = S->m; a.mode = GEMV_CERT; a.out_c = S->c; a.out_t = S->t;
-        a.blk_val = S->s.blk_val; a.blk_idx = S->s.blk_idx; a.norms = M->norms; a.beta = S->beta;
-        a.lam = S->hs->lam; a.rho_norm_dev = &S->sc->rho_norm_ub; a.gam = gamma_n(M->sparse ? 64 : M->n);
-        if (M->sparse) {
-            // CSC columns are short; bound with the true max column length
-            a.gam = gamma_n(std::min<int64_t>(M->n, M->nnz));
-        }
-        TRY(launch_gemv(M, S->st, a, nullptr));
-    }
-    CdArgs c{};
-    c.ld = M->ld; c.n = (int)M->n; c.A = S->A; c.m = S->m; c.tcert = certify ? S->t : nullptr;
-    c.beta = S->beta; c.rho = S->rho; c.nsq = M->norms_sq; c.norms = M->norms; c.lam = S->hs->lam; c.sc = S->sc;
-    return launch_cd(M, S->st, c);
-}
-
-static int copy_active_host(gs_solver* S, int64_t* out) {
-    std::vector<int32_t> tmp(std::max<int64_t>(S->m, 1));
-    if (S->m) CK(cudaMemcpyAsync(tmp.data(), S->A, S->m * 4, cudaMemcpyDeviceToHost, S->st));
+static int copy_active_host(gs_solver* S, int64_t m, int64_t* out) {
+    std::vector<int32_t> tmp(std::max<int64_t>(m, 1));
+    if (m) CK(cudaMemcpyAsync(tmp.data(), S->A, m * 4, cudaMemcpyDeviceToHost, S->st));
     CK(cudaStreamSynchronize(S->st));
-    for (int64_t i = 0; i < S->m; ++i) out[i] = tmp[i];
+    for (int64_t i = 0; i < m; ++i) out[i] = tmp[i];
     return GS_OK;
 }
 
-static int fire_hook(gs_solver* S, const gs_solve_config* cfg) {
-    if (!cfg->on_checkpoint) return GS_OK;
-    std::vector<int64_t> act(std::max<int64_t>(S->m, 1));
-    TRY(copy_active_host(S, act.data()));
-    cfg->on_checkpoint(act.data(), S->m, cfg->user);
-    return GS_OK;
-}
-
-// screen all p with a sphere whose radius lives in sc->radius (seq screen)
-// or is given (lambda_max shortcut, radius 0); result into S->A, count sc->m.
-static int screen_all(gs_solver* S, const double* center, const double* radius_dev, double radius_host) {
-    GemvArgs a{};
-    a.v = center; a.m = S->p; a.mode = GEMV_MU; a.scale = 1.0; a.radius_dev = radius_dev;
-    a.radius_host = radius_host; a.thresh = 1.0 - 1e-9; a.norms = S->M->norms; a.flags = S->flags;
-    TRY(launch_gemv(S->M, S->st, a, nullptr));
-    TRY(launch_compact(S->st, S->s, S->flags, S->p, nullptr, S->A, &S->sc->m));
-    return GS_OK;
-}
-
+// Sequential screen of path.py:82-91: runs fused at the start of the next
+// solve (init_mode 2) from the device-resident previous (beta, theta, rho).
 extern "C" int gs_solver_seq_screen(gs_solver* S, double lam, int64_t* n_active) {
     if (!S->has_prev) return fail(GS_ERR_VALUE, "sequential screen needs a previous solve");
-    S->hs->lam = lam;
-    TRY(sc_upload(S));
-    k_seq_gap<<<1, 1024, 0, S->st>>>(S->rho, S->y, S->theta, (int)S->n, S->beta, S->A, S->m, S->prev_margin, S->sc);
-    CKL();
-    TRY(screen_all(S, S->theta, &S->sc->radius, 0.0));
-    TRY(sc_download(S));
-    if (S->hs->status != ST_OK) {
-        S->hs->margin = S->prev_margin;
-        return status_error(S->hs->status, S->hs, true);
-    }
-    S->m = S->hs->m;
-    *n_active = S->m;
+    S->seq_pending = true;
+    S->seq_lam = lam;
+    if (n_active) *n_active = -1;
     return GS_OK;
 }
 
-static int solve_outputs(gs_solver* S, gs_solve_result* R, int64_t n_trace) {
+static int solve_outputs(gs_solver* S, gs_solve_result* R, int64_t n_trace, int64_t m) {
     cudaStream_t st = S->st;
     if (R->beta) CK(cudaMemcpyAsync(R->beta, S->beta, S->p * 8, cudaMemcpyDeviceToHost, st));
     if (R->residual) CK(cudaMemcpyAsync(R->residual, S->rho, S->n * 8, cudaMemcpyDeviceToHost, st));
     if (R->theta) CK(cudaMemcpyAsync(R->theta, S->theta, S->n * 8, cudaMemcpyDeviceToHost, st));
-    if (R->active) TRY(copy_active_host(S, R->active));
+    if (R->active) TRY(copy_active_host(S, m, R->active));
     std::vector<TraceRow> tr(std::max<int64_t>(n_trace, 1));
     if (n_trace > 0 && S->trace)
         CK(cudaMemcpyAsync(tr.data(), S->trace, n_trace * sizeof(TraceRow), cudaMemcpyDeviceToHost, st));
@@ -739,7 +767,7 @@ static int solve_outputs(gs_solver* S, gs_solve_result* R, int64_t n_trace) {
         if (R->trace_radius) R->trace_radius[i] = tr[i].radius;
     }
     R->n_trace = n_trace;
-    R->n_active = S->m;
+    R->n_active = m;
     return GS_OK;
 }
 
@@ -752,49 +780,78 @@ static int ensure_trace(gs_solver* S, int64_t rows) {
     return GS_OK;
 }
 
+static void fill_dev(gs_solver* S, SolveDev& d) {
+    const gs_matrix* M = S->M;
+    memset(&d, 0, sizeof d);
+    d.X = M->X; d.ld = M->ld; d.n = (int)M->n; d.dtype = M->dtype; d.p = M->p; d.sparse = M->sparse;
+    d.data = M->data; d.indices = M->indices; d.indptr = M->indptr;
+    d.csr_data = M->csr_data; d.csr_cols = M->csr_cols; d.csr_rowptr = M->csr_rowptr;
+    d.norms = M->norms; d.nsq = M->norms_sq;
+    d.y = S->y; d.beta = S->beta; d.rho = S->rho; d.theta = S->theta; d.c = S->c; d.t = S->t; d.t2 = S->t2;
+    d.A = S->A; d.A2 = S->A2; d.S = S->S; d.Dl = S->Dl; d.mark = S->mark;
+    d.partial = S->partial; d.nch_max = S->nch_max;
+    d.sc = S->sc; d.ctl = S->ctl; d.trace = S->trace; d.trace_cap = S->trace_cap; d.bar = S->bar;
+    d.cta_val = S->cta_val; d.cta_idx = S->cta_idx; d.cta_cnt = S->cta_cnt;
+    const CdShape cs = cd_shape(M->n);
+    d.cd_warps = M->sparse ? 1 : cs.W;
+    d.vs_cap = vs_cap_for(M);
+    const char* env = getenv("GS_REFRESH_EXCESS");
+    d.refresh_excess = env ? atoi(env) : 32;
+}
+
 extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* cfg, const int64_t* active0,
                                int64_t n0, int active0_mode, gs_solve_result* R) {
     if (!(lam > 0)) return fail(GS_ERR_VALUE, "lambda must be positive");
     if (cfg->epsilon <= 0) return fail(GS_ERR_VALUE, "epsilon must be positive");
     if (cfg->screen_every < 1) return fail(GS_ERR_VALUE, "screen_every must be at least 1");
     if (cfg->max_passes < 1) return fail(GS_ERR_VALUE, "max_passes must be at least 1");
+    if (active0_mode == 2 && !(S->seq_pending && S->seq_lam == lam))
+        return fail(GS_ERR_VALUE, "active0_mode 2 needs gs_solver_seq_screen at the same lambda");
+    S->seq_pending = false;
     const gs_matrix* M = S->M;
     cudaStream_t st = S->st;
     const int64_t p = S->p;
     const bool gap_rule = cfg->rule == GS_RULE_GAP_SPHERE;
-    const bool certify = cfg->certify != 0;
     const int64_t f = cfg->screen_every;
     TRY(ensure_trace(S, cfg->max_passes / f + 4));
     DevScalars* h = S->hs;
     h->lam = lam; h->eps = cfg->epsilon; h->y_norm_sq = S->y_norm_sq;
     h->visits = h->uncertified = h->nonzero = 0;
     h->status = ST_OK;
-    TRY(sc_upload(S));
+    h->m = S->m;
     CK(cudaEventRecord(S->ev0, st));
     memset(&R->n_active, 0, sizeof(gs_solve_result) - offsetof(gs_solve_result, n_active));
 
     // ---- lambda >= lambda_max: _solve_at_lambda_max (solver.py:129-146, 160-161)
     if (lam >= S->lmax * (1 - 1e-14)) {
+        TRY(sc_upload(S));
         CK(cudaMemsetAsync(S->beta, 0, p * 8, st));
         CK(cudaMemcpyAsync(S->rho, S->y, S->n * 8, cudaMemcpyDeviceToDevice, st));
         k_scale_vec<<<grid_for(S->n, 256), 256, 0, st>>>(S->y, lam, S->n, S->theta, 1);
         CKL();
         if (gap_rule) {
-            TRY(screen_all(S, S->theta, nullptr, 0.0));
+            GemvArgs a{};
+            a.v = S->theta; a.m = p; a.mode = GEMV_MU; a.scale = 1.0; a.radius_host = 0.0;
+            a.thresh = 1.0 - 1e-9; a.norms = M->norms; a.flags = S->flags;
+            TRY(launch_gemv(M, st, a, nullptr));
         } else {
             k_flags_norm_pos<<<grid_for(p, 256), 256, 0, st>>>(nullptr, p, M->norms, S->flags);
             CKL();
-            TRY(launch_compact(st, S->s, S->flags, p, nullptr, S->A, &S->sc->m));
         }
+        TRY(launch_compact(st, S->s, S->flags, p, nullptr, S->A, &S->sc->m));
         TRY(sc_download(S));
         S->m = h->m;
         TraceRow row{0, S->m, 0.0, 0.0};
         CK(cudaMemcpyAsync(S->trace, &row, sizeof row, cudaMemcpyHostToDevice, st));
-        TRY(fire_hook(S, cfg));
+        if (cfg->on_checkpoint) {
+            std::vector<int64_t> act(std::max<int64_t>(S->m, 1));
+            TRY(copy_active_host(S, S->m, act.data()));
+            cfg->on_checkpoint(act.data(), S->m, cfg->user);
+        }
         R->converged = 1; R->margin = 0.0; R->interpolating = 0; R->lambda_max_shortcut = 1;
         R->primal = 0.5 * S->y_norm_sq; R->dual = 0.5 * S->y_norm_sq; R->gap = 0.0;
         R->passes_done = 0; R->checkpoints = 0;
-        TRY(solve_outputs(S, R, 1));
+        TRY(solve_outputs(S, R, 1, S->m));
         S->has_prev = true; S->prev_margin = 0.0; S->prev_interp = 0;
         CK(cudaEventRecord(S->ev1, st));
         CK(cudaEventSynchronize(S->ev1));
@@ -803,114 +860,58 @@ extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* 
         return GS_OK;
     }
 
-    // ---- active set init (solver.py:171-178): active0 filtered to nonzero norms
+    // ---- the persistent solve
     if (active0_mode == 1) {
-        TmpBuf tb;
-        int32_t* d0 = nullptr;
-        if (n0 > 0) {
-            TRY(upload_cols(st, tb, M, active0, n0, &d0));
-            CK(cudaMemcpyAsync(S->A2, d0, n0 * 4, cudaMemcpyDeviceToDevice, st));
+        std::vector<int32_t> c32(std::max<int64_t>(n0, 1));
+        for (int64_t i = 0; i < n0; ++i) {
+            if (active0[i] < 0 || active0[i] >= p) return fail(GS_ERR_INDEX, "active0 index out of range");
+            c32[i] = (int32_t)active0[i];
         }
-        k_flags_norm_pos<<<grid_for(std::max<int64_t>(n0, 1), 256), 256, 0, st>>>(S->A2, n0, M->norms, S->flags);
-        CKL();
-        TRY(launch_compact(st, S->s, S->flags, n0, S->A2, S->A, &S->sc->m));
-        CK(cudaStreamSynchronize(st));
-    } else if (active0_mode == 2) {
-        const int64_t m0 = S->m;
-        k_flags_norm_pos<<<grid_for(std::max<int64_t>(m0, 1), 256), 256, 0, st>>>(S->A, m0, M->norms, S->flags);
-        CKL();
-        TRY(launch_compact(st, S->s, S->flags, m0, S->A, S->A2, &S->sc->m));
-        std::swap(S->A, S->A2);
-    } else {
-        k_flags_norm_pos<<<grid_for(p, 256), 256, 0, st>>>(nullptr, p, M->norms, S->flags);
-        CKL();
-        TRY(launch_compact(st, S->s, S->flags, p, nullptr, S->A, &S->sc->m));
+        if (n0) CK(cudaMemcpyAsync(S->A2, c32.data(), n0 * 4, cudaMemcpyHostToDevice, st));
+        h->cnt = n0;
     }
-    CK(cudaMemcpyAsync(&S->hs->m, &S->sc->m, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    S->m = h->m;
-    if (S->m > 0) {
-        k_set_mark<<<grid_for(S->m, 256), 256, 0, st>>>(S->A, S->m, S->mark);
-        CKL();
-    }
-    k_zero_unmarked<<<grid_for(p, 256), 256, 0, st>>>(S->beta, S->mark, p);
-    CKL();
-
-    int64_t passes = 0, ntrace = 0, nckpt = 0;
-    bool converged = false;
-    const double thresh = 1.0 - 1e-9;
-    for (int64_t k = 1; k <= cfg->max_passes; ++k) {
-        if (f == 1 || k % f == 1) {
-            ++nckpt;
-            TRY(resync(S));
-            if (S->m == 0) {
-                // everything screened: unrestricted dual point (solver.py:190-203)
-                TRY(dual_corr(S, false));
-                k_ckpt_dual<<<1, 1024, 0, st>>>(S->rho, S->y, (int)S->n, S->beta, S->A, 0, S->theta, S->sc, 0);
-                CKL();
-                k_ckpt_post<<<1, 1024, 0, st>>>(S->rho, (int)S->n, S->beta, S->A, S->sc, S->trace, ntrace, passes);
-                CKL();
-                TRY(sc_download(S));
-                if (h->status != ST_OK) return status_error(h->status, h, false);
-                ++ntrace;
-                TRY(fire_hook(S, cfg));
-                converged = h->gap_post <= cfg->epsilon;
-                break;
-            }
-            TRY(dual_corr(S, true));
-            k_ckpt_dual<<<1, 1024, 0, st>>>(S->rho, S->y, (int)S->n, S->beta, S->A, S->m, S->theta, S->sc, gap_rule ? 1 : 0);
-            CKL();
-            if (gap_rule) {
-                k_ckpt_keep<<<grid_for(S->m, 256), 256, 0, st>>>(S->c, S->A, S->m, M->norms, S->beta, S->sc, thresh, S->flags, S->flags2);
-                CKL();
-                TRY(launch_compact(st, S->s, S->flags2, S->m, S->A, S->Dl, &S->sc->n_drop));
-                if (M->sparse)
-                    k_drop_axpy_csc<<<1, 256, 0, st>>>(M->data, M->indices, M->indptr, S->Dl, &S->sc->n_drop, S->beta, S->rho);
-                else if (M->dtype == GS_DTYPE_F64)
-                    k_drop_axpy_dense<double><<<(unsigned)((S->n + 255) / 256), 256, 0, st>>>((const double*)M->X, M->ld, (int)S->n, S->Dl, &S->sc->n_drop, S->beta, S->rho);
-                else
-                    k_drop_axpy_dense<float><<<(unsigned)((S->n + 255) / 256), 256, 0, st>>>((const float*)M->X, M->ld, (int)S->n, S->Dl, &S->sc->n_drop, S->beta, S->rho);
-                k_zero_listed<<<grid_for(S->m, 256), 256, 0, st>>>(S->beta, S->Dl, &S->sc->n_drop);
-                CKL();
-                TRY(launch_compact(st, S->s, S->flags, S->m, S->A, S->A2, &S->sc->m));
-                std::swap(S->A, S->A2);
-            }
-            k_ckpt_post<<<1, 1024, 0, st>>>(S->rho, (int)S->n, S->beta, S->A, S->sc, S->trace, ntrace, passes);
-            CKL();
-            TRY(sc_download(S));
-            if (h->status != ST_OK) return status_error(h->status, h, false);
-            S->m = h->m;
-            ++ntrace;
-            TRY(fire_hook(S, cfg));
-            if (h->gap_post <= cfg->epsilon) { converged = true; break; }
-            if (S->m == 0) break;
-        } else if (k % 100 == 0) {
-            TRY(resync(S));
-            k_rho_norm_ub<<<1, 1024, 0, st>>>(S->rho, (int)S->n, S->sc);
-            CKL();
-        }
-        TRY(cd_epoch(S, certify));
-        ++passes;
-    }
-    double primal, dual, gap;
-    if (!converged) {
-        // budget exhausted or early break: certify the final iterate (solver.py:237-245)
-        TRY(resync(S));
-        TRY(dual_corr(S, S->m > 0));
-        k_ckpt_dual<<<1, 1024, 0, st>>>(S->rho, S->y, (int)S->n, S->beta, S->A, S->m, S->theta, S->sc, 0);
-        CKL();
+    TRY(sc_upload(S));
+    memset(S->hctl, 0, sizeof(SolveCtl));
+    CK(cudaMemcpyAsync(S->ctl, S->hctl, sizeof(SolveCtl), cudaMemcpyHostToDevice, st));
+    SolveDev d;
+    fill_dev(S, d);
+    d.lam = lam; d.eps = cfg->epsilon; d.max_passes = cfg->max_passes; d.f = f;
+    d.rule = cfg->rule; d.certify = cfg->certify; d.stop_at_ckpt = cfg->on_checkpoint ? 1 : 0;
+    d.init_mode = active0_mode == 2 ? 2 : (active0_mode == 1 ? 1 : 0);
+    d.prev_margin = S->prev_margin;
+    CK(cudaMemcpyAsync(S->dprob, &d, sizeof d, cudaMemcpyHostToDevice, st));
+    const size_t smem = solve_smem(M);
+    const int Rr = M->sparse ? 1 : cd_shape(M->n).R;
+    int64_t hook_fired = 0, launches = 0;
+    while (true) {
+        TRY(launch_solve(M, st, S->dprob, S->G, 1, smem, Rr));
+        ++launches;
         TRY(sc_download(S));
-        if (h->status != ST_OK) return status_error(h->status, h, false);
-        primal = h->primal; dual = h->dual; gap = h->gap_pre;
-        converged = gap <= cfg->epsilon;
-    } else {
-        primal = h->primal_post; dual = h->dual; gap = h->gap_post;
+        const SolveCtl* c = S->hctl;
+        if (h->status != ST_OK) {
+            S->has_prev = false;
+            return status_error(h->status, h->margin, h->gap_pre);
+        }
+        if (cfg->on_checkpoint && c->nckpt > hook_fired) {
+            std::vector<int64_t> act(std::max<int64_t>(h->m, 1));
+            TRY(copy_active_host(S, h->m, act.data()));
+            cfg->on_checkpoint(act.data(), h->m, cfg->user);
+            hook_fired = c->nckpt;
+        }
+        if (c->done) break;
     }
-    R->converged = converged; R->margin = h->margin; R->interpolating = h->interp;
-    R->primal = primal; R->dual = dual; R->gap = gap;
-    R->passes_done = passes; R->checkpoints = nckpt;
+    const SolveCtl* c = S->hctl;
+    S->m = h->m;
+    R->converged = c->converged;
+    R->margin = h->margin; R->interpolating = h->interp;
+    if (c->final_done) { R->primal = h->primal; R->dual = h->dual; R->gap = h->gap_pre; }
+    else { R->primal = h->primal_post; R->dual = h->dual; R->gap = h->gap_post; }
+    R->passes_done = c->passes; R->checkpoints = c->nckpt;
     R->cd_visits = h->visits; R->cd_uncertified = h->uncertified; R->cd_nonzero = h->nonzero;
-    TRY(solve_outputs(S, R, ntrace));
+    R->screen_ms = c->t_screen * 1e-6; R->ckpt_ms = c->t_ckpt * 1e-6;
+    R->refresh_ms = c->t_refresh * 1e-6; R->cd_ms = c->t_cd * 1e-6;
+    R->n_screen = c->n_screen; R->n_refresh = c->n_refresh; R->launches = launches;
+    TRY(solve_outputs(S, R, c->ntrace, S->m));
     S->has_prev = true; S->prev_margin = h->margin; S->prev_interp = h->interp;
     CK(cudaEventRecord(S->ev1, st));
     CK(cudaEventSynchronize(S->ev1));
@@ -953,27 +954,24 @@ extern "C" int gs_cd_pass(const gs_matrix* M, double* beta, double* rho, const i
                 k_cd_pass_exact_dense<float><<<1, 256, 0, st>>>((const float*)M->X, M->ld, (int)n, db, dr, dA, k, lam, dns, tail_scale);
             CKL();
         } else {
-            // production path: certification anchor at the incoming rho
-            DevScalars* sc; double *c, *t;
-            TRY(tb.get(&sc, 1)); TRY(tb.get(&c, k)); TRY(tb.get(&t, k));
-            CK(cudaMemsetAsync(sc, 0, sizeof(DevScalars), st));
-            k_rho_norm_ub<<<1, 1024, 0, st>>>(dr, (int)n, sc);
-            Scratch s;
-            TRY(s.alloc(k));
-            GemvArgs a{};
-            a.v = dr; a.cols = dA; a.m = k; a.mode = GEMV_CERT; a.out_c = c; a.out_t = t;
-            a.blk_val = s.blk_val; a.blk_idx = s.blk_idx; a.norms = dnorm; a.beta = db; a.lam = lam;
-            a.rho_norm_dev = &sc->rho_norm_ub; a.gam = gamma_n(n);
-            int rc = launch_gemv(M, st, a, nullptr);
-            if (rc == GS_OK) {
-                CdArgs cda{};
-                cda.ld = M->ld; cda.n = (int)n; cda.A = dA; cda.m = k; cda.tcert = t; cda.beta = db; cda.rho = dr;
-                cda.nsq = dns; cda.norms = dnorm; cda.lam = lam; cda.sc = sc;
-                rc = launch_cd(M, st, cda);
-            }
-            CK(cudaStreamSynchronize(st));
-            s.release();
-            if (rc != GS_OK) return rc;
+            TRY(check_shape(M));
+            DevScalars* sc; SolveCtl* ctl; double* c; float* t; SolveDev* dp; double* cval; int64_t* cidx;
+            TRY(tb.get(&sc, 1)); TRY(tb.get(&ctl, 1)); TRY(tb.get(&c, k)); TRY(tb.get(&t, k)); TRY(tb.get(&dp, 1));
+            TRY(tb.get(&cval, 1)); TRY(tb.get(&cidx, 1));
+            DevScalars hs{};
+            hs.m = k;
+            CK(cudaMemcpyAsync(sc, &hs, sizeof hs, cudaMemcpyHostToDevice, st));
+            CK(cudaMemsetAsync(ctl, 0, sizeof(SolveCtl), st));
+            SolveDev d;
+            memset(&d, 0, sizeof d);
+            d.X = M->X; d.ld = M->ld; d.n = (int)n; d.dtype = M->dtype; d.p = p; d.sparse = M->sparse;
+            d.data = M->data; d.indices = M->indices; d.indptr = M->indptr;
+            d.norms = dnorm; d.nsq = dns; d.beta = db; d.rho = dr; d.c = c; d.t = t; d.A = dA;
+            d.sc = sc; d.ctl = ctl; d.lam = lam; d.certify = 1; d.cta_val = cval; d.cta_idx = cidx;
+            d.cd_warps = M->sparse ? 1 : cd_shape(n).W;
+            d.vs_cap = vs_cap_for(M);
+            CK(cudaMemcpyAsync(dp, &d, sizeof d, cudaMemcpyHostToDevice, st));
+            TRY(launch_cdpass(M, st, dp, solve_smem(M), M->sparse ? 1 : cd_shape(n).R));
         }
     }
     CK(cudaMemcpyAsync(beta, db, p * 8, cudaMemcpyDeviceToHost, st));
@@ -1021,3 +1019,79 @@ extern "C" int gs_screen_sphere(const gs_matrix* M, const double* center, double
     s.release();
     return rc;
 }
+
+// ---------------------------------------------------------------------------
+// measurement support
+// ---------------------------------------------------------------------------
+extern "C" int gs_solver_timer(gs_solver* S, int op, double* ms) {
+    if (op == 0) {
+        CK(cudaStreamSynchronize(S->st));
+        CK(cudaEventRecord(S->tev0, S->st));
+        return GS_OK;
+    }
+    CK(cudaEventRecord(S->tev1, S->st));
+    CK(cudaEventSynchronize(S->tev1));
+    float f = 0.0f;
+    CK(cudaEventElapsedTime(&f, S->tev0, S->tev1));
+    if (ms) *ms = f;
+    return GS_OK;
+}
+
+extern "C" int gs_screen_timed(const gs_matrix* M, const double* center, double radius, int reps, double* ms,
+                               int64_t* n_active) {
+    TRY(ensure_device());
+    if (reps < 1) reps = 1;
+    cudaStream_t st = M->st;
+    TmpBuf tb;
+    double* dv; uint8_t* mark; int32_t* out; int64_t* cnt; SolveDev* dp;
+    TRY(tb.get(&dv, M->n + 2)); TRY(tb.get(&mark, M->p)); TRY(tb.get(&out, M->p)); TRY(tb.get(&cnt, 1));
+    TRY(tb.get(&dp, 1));
+    CK(cudaMemcpyAsync(dv, center, M->n * 8, cudaMemcpyHostToDevice, st));
+    SolveDev d;
+    memset(&d, 0, sizeof d);
+    d.X = M->X; d.ld = M->ld; d.n = (int)M->n; d.dtype = M->dtype; d.p = M->p; d.sparse = M->sparse;
+    d.data = M->data; d.indices = M->indices; d.indptr = M->indptr; d.norms = M->norms; d.nsq = M->norms_sq;
+    d.theta = dv; d.mark = mark; d.vs_cap = vs_cap_for(M);
+    CK(cudaMemcpyAsync(dp, &d, sizeof d, cudaMemcpyHostToDevice, st));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = solve_smem(M);
+    Scratch s;
+    TRY(s.alloc(M->p));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    int rc = GS_OK;
+    const bool f64 = M->sparse || M->dtype == GS_DTYPE_F64;
+    if (f64) CK(cudaFuncSetAttribute(k_screen_full<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    else CK(cudaFuncSetAttribute(k_screen_full<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto one = [&]() -> int {
+        COUNT_LAUNCH(1);
+        if (f64) k_screen_full<double><<<sms, kSolveThreads, smem, st>>>(dp, radius);
+        else k_screen_full<float><<<sms, kSolveThreads, smem, st>>>(dp, radius);
+        CKL();
+        return launch_compact(st, s, mark, M->p, nullptr, out, cnt);
+    };
+    rc = one();   // warm-up
+    if (rc == GS_OK) {
+        CK(cudaEventRecord(e0, st));
+        for (int r = 0; r < reps && rc == GS_OK; ++r) rc = one();
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        float f = 0.0f;
+        cudaEventElapsedTime(&f, e0, e1);
+        *ms = f / reps;
+        CK(cudaMemcpy(n_active, cnt, 8, cudaMemcpyDeviceToHost));
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    s.release();
+    return rc;
+}
+
+extern "C" int gs_host_alloc(int64_t bytes, void** out) {
+    TRY(ensure_device());
+    CK(cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1)));
+    return GS_OK;
+}
+
+extern "C" void gs_host_free(void* ptr) { cudaFreeHost(ptr); }

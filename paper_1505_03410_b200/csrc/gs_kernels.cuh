@@ -39,6 +39,8 @@ struct DevScalars {
     unsigned long long visits, uncertified, nonzero;
 };
 
+struct TraceRow { int64_t passes, n_active; double gap, radius; };
+
 enum Status : int32_t {
     ST_OK = 0,
     ST_INFEASIBLE = 1,     // InfeasibleDualError   (problem.py:74-76)
@@ -58,7 +60,7 @@ template <> struct ColDot<double> {
         const double2* v2 = reinterpret_cast<const double2*>(v);
         const int n2 = n >> 1;
         double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
+#pragma unroll 8
         for (int q = lane; q < n2; q += kWarp) {
             const double2 xv = __ldg(x2 + q);
             const double2 vv = v2[q];
@@ -89,6 +91,83 @@ template <> struct ColDot<float> {
         }
         for (int r = (n4 << 2) + lane; r < n; r += kWarp) a0 = fma((double)__ldg(x + r), v[r], a0);
         return warp_sum(a0 + a1);
+    }
+};
+
+
+// two columns per warp in flight (doubles the bytes in flight per warp);
+// per-column summation order identical to ColDot<T>::run.
+template <typename T> struct ColDot2;
+
+template <> struct ColDot2<double> {
+    static __device__ __forceinline__ void run(const double* __restrict__ x0, const double* __restrict__ x1,
+                                               const double* __restrict__ v, int n, int lane, double& c0,
+                                               double& c1) {
+        const double2* p0 = reinterpret_cast<const double2*>(x0);
+        const double2* p1 = reinterpret_cast<const double2*>(x1);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const int n2 = n >> 1;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n2; q += kWarp) {
+            const double2 xa = __ldg(p0 + q);
+            const double2 xb = __ldg(p1 + q);
+            const double2 vv = v2[q];
+            a0 = fma(xa.x, vv.x, a0);
+            a1 = fma(xa.y, vv.y, a1);
+            b0 = fma(xb.x, vv.x, b0);
+            b1 = fma(xb.y, vv.y, b1);
+        }
+        if ((n & 1) && lane == 0) {
+            a0 = fma(__ldg(x0 + n - 1), v[n - 1], a0);
+            b0 = fma(__ldg(x1 + n - 1), v[n - 1], b0);
+        }
+        double s0 = a0 + a1, s1 = b0 + b1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        c0 = s0;
+        c1 = s1;
+    }
+};
+
+template <> struct ColDot2<float> {
+    static __device__ __forceinline__ void run(const float* __restrict__ x0, const float* __restrict__ x1,
+                                               const double* __restrict__ v, int n, int lane, double& c0,
+                                               double& c1) {
+        const float4* p0 = reinterpret_cast<const float4*>(x0);
+        const float4* p1 = reinterpret_cast<const float4*>(x1);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const int n4 = n >> 2;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n4; q += kWarp) {
+            const float4 xa = __ldg(p0 + q);
+            const float4 xb = __ldg(p1 + q);
+            const double2 va = v2[2 * q], vb = v2[2 * q + 1];
+            a0 = fma((double)xa.x, va.x, a0);
+            a1 = fma((double)xa.y, va.y, a1);
+            a0 = fma((double)xa.z, vb.x, a0);
+            a1 = fma((double)xa.w, vb.y, a1);
+            b0 = fma((double)xb.x, va.x, b0);
+            b1 = fma((double)xb.y, va.y, b1);
+            b0 = fma((double)xb.z, vb.x, b0);
+            b1 = fma((double)xb.w, vb.y, b1);
+        }
+        for (int r = (n4 << 2) + lane; r < n; r += kWarp) {
+            a0 = fma((double)__ldg(x0 + r), v[r], a0);
+            b0 = fma((double)__ldg(x1 + r), v[r], b0);
+        }
+        double s0 = a0 + a1, s1 = b0 + b1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        c0 = s0;
+        c1 = s1;
     }
 };
 
@@ -419,76 +498,6 @@ __global__ void k_resync_csr(const double* __restrict__ data, const int32_t* __r
     out[r] = y ? y[r] - s : s;
 }
 
-// ---------------------------------------------------------------------------
-// checkpoint scalar algebra (single block)
-// ---------------------------------------------------------------------------
-// Eq. 10 dual point and pre-drop certificate (problem.py:98-123, 57-86;
-// regions.py:213-218).  restricted m = |X_A^T rho|_inf arrives in sc->corr.
-__global__ void __launch_bounds__(1024) k_ckpt_dual(const double* __restrict__ rho, const double* __restrict__ y,
-                                                    int n, const double* __restrict__ beta,
-                                                    const int32_t* __restrict__ A, int64_t m,
-                                                    double* __restrict__ theta, DevScalars* sc, int want_radius) {
-    __shared__ double red[32];
-    const double lam = sc->lam;
-    double a = 0.0, b = 0.0;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) { const double q = rho[r]; a = fma(q, q, a); b = fma(y[r], q, b); }
-    const double rho_sq = block_sum(a, red);
-    const double y_rho = block_sum(b, red);
-    const double corr = sc->corr;
-    double alpha = 0.0, margin = 1.0;
-    int interp = 0;
-    if (rho_sq == 0.0) {
-        interp = 1;
-    } else {
-        const double raw = y_rho / (lam * rho_sq);
-        if (corr > 0.0) {
-            const double bound = 1.0 / corr;
-            alpha = fmin(fmax(raw, -bound), bound);
-        } else {
-            alpha = raw;
-        }
-        margin = 1.0 - fabs(alpha) * corr;
-    }
-    double dd = 0.0, l1 = 0.0;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) {
-        const double th = interp ? 0.0 : alpha * rho[r];
-        theta[r] = th;
-        const double diff = th - y[r] / lam;
-        dd = fma(diff, diff, dd);
-    }
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) l1 += fabs(beta[A[i]]);
-    const double dsq = block_sum(dd, red);
-    const double l1s = block_sum(l1, red);
-    if (threadIdx.x == 0) {
-        const double dual = 0.5 * sc->y_norm_sq - 0.5 * (lam * lam) * dsq;
-        const double primal = 0.5 * rho_sq + lam * l1s;
-        const double gap = primal - dual;
-        sc->rho_sq = rho_sq; sc->y_rho = y_rho; sc->alpha = alpha; sc->margin = margin; sc->interp = interp;
-        sc->l1 = l1s; sc->primal = primal; sc->dual = dual; sc->gap_pre = gap;
-        int st = ST_OK;
-        if (margin < -1e-9) st = ST_INFEASIBLE;
-        else if (want_radius && gap < -1e-10) st = ST_NEG_GAP;
-        sc->status = st;
-        sc->radius = sqrt(2.0 * fmax(gap, 0.0)) / lam;
-    }
-}
-
-// mu_A from the stored restricted dots: mu_i = |alpha c_i| + r ||x_{A_i}||,
-// keep = mu >= 1 - tol (solver.py:208-209); drop_nz = !keep && beta != 0.
-__global__ void k_ckpt_keep(const double* __restrict__ c, const int32_t* __restrict__ A, int64_t m,
-                            const double* __restrict__ norms, const double* __restrict__ beta,
-                            const DevScalars* __restrict__ sc, double thresh,
-                            uint8_t* __restrict__ keep, uint8_t* __restrict__ drop_nz) {
-    const double alpha = sc->alpha, r = sc->radius;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t j = A[i];
-        const double mu = fabs(alpha * c[i]) + r * norms[j];
-        const bool k = mu >= thresh;
-        keep[i] = k;
-        drop_nz[i] = (!k) && beta[j] != 0.0;
-    }
-}
-
 // rho += beta_j x_j for dropped j in ascending order (numpy: v += a * x,
 // separate roundings), thread per row.
 template <typename T>
@@ -522,49 +531,6 @@ __global__ void k_drop_axpy_csc(const double* __restrict__ data, const int32_t* 
     }
 }
 
-__global__ void k_zero_listed(double* __restrict__ beta, const int32_t* __restrict__ D,
-                              const int64_t* __restrict__ d_count) {
-    const int64_t nd = *d_count;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nd; k += (int64_t)gridDim.x * blockDim.x)
-        beta[D[k]] = 0.0;
-}
-
-// post-drop certificate with the same theta (solver.py:217-221), trace row.
-struct TraceRow { int64_t passes, n_active; double gap, radius; };
-
-__global__ void __launch_bounds__(1024) k_ckpt_post(const double* __restrict__ rho, int n,
-                                                    const double* __restrict__ beta,
-                                                    const int32_t* __restrict__ A, DevScalars* sc,
-                                                    TraceRow* trace, int64_t trace_pos, int64_t passes) {
-    __shared__ double red[32];
-    const double lam = sc->lam;
-    const int64_t m = sc->m;
-    double a = 0.0, aru = 0.0, l1 = 0.0;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) { const double q = rho[r]; a = fma(q, q, a); aru = __dadd_ru(aru, __dmul_ru(q, q)); }
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) l1 += fabs(beta[A[i]]);
-    const double rho_sq = block_sum(a, red);
-    const double rho_sq_ru = block_sum_ru(aru, red);
-    const double l1s = block_sum(l1, red);
-    if (threadIdx.x == 0) {
-        const double primal = 0.5 * rho_sq + lam * l1s;
-        const double gap = primal - sc->dual;
-        sc->primal_post = primal;
-        sc->gap_post = gap;
-        sc->radius_post = sqrt(2.0 * fmax(gap, 0.0)) / lam;
-        sc->rho_norm_ub = __dsqrt_ru(rho_sq_ru);
-        if (trace) trace[trace_pos] = TraceRow{passes, m, gap, sc->radius_post};
-    }
-}
-
-// rigorous upper bound of ||rho|| (certification anchor after a resync).
-__global__ void __launch_bounds__(1024) k_rho_norm_ub(const double* __restrict__ rho, int n, DevScalars* sc) {
-    __shared__ double red[32];
-    double a = 0.0;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) { const double q = rho[r]; a = __dadd_ru(a, __dmul_ru(q, q)); }
-    const double s = block_sum_ru(a, red);
-    if (threadIdx.x == 0) sc->rho_norm_ub = __dsqrt_ru(s);
-}
-
 // generic dot / abs-sum over device vectors (problem.py scalar algebra for
 // the drop-in helper functions).  out[0] = sum a*b, out[1] = sum |a|.
 __global__ void __launch_bounds__(1024) k_vec_stats(const double* __restrict__ a, const double* __restrict__ b,
@@ -579,217 +545,6 @@ __global__ void __launch_bounds__(1024) k_vec_stats(const double* __restrict__ a
     s = block_sum(s, red);
     t = block_sum(t, red);
     if (threadIdx.x == 0) { out[0] = s; out[1] = t; }
-}
-
-// sequential-screen gap at a new lambda for the previous pair (path.py:82-91,
-// regions.py:221-232).  Reads previous beta over the previous active set.
-__global__ void __launch_bounds__(1024) k_seq_gap(const double* __restrict__ rho, const double* __restrict__ y,
-                                                  const double* __restrict__ theta, int n,
-                                                  const double* __restrict__ beta, const int32_t* __restrict__ A,
-                                                  int64_t m, double prev_margin, DevScalars* sc) {
-    __shared__ double red[32];
-    const double lam = sc->lam;
-    double a = 0.0, dd = 0.0, l1 = 0.0;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) {
-        const double q = rho[r];
-        a = fma(q, q, a);
-        const double diff = theta[r] - y[r] / lam;
-        dd = fma(diff, diff, dd);
-    }
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) l1 += fabs(beta[A[i]]);
-    const double rho_sq = block_sum(a, red);
-    const double dsq = block_sum(dd, red);
-    const double l1s = block_sum(l1, red);
-    if (threadIdx.x == 0) {
-        const double primal = 0.5 * rho_sq + lam * l1s;
-        const double dual = 0.5 * sc->y_norm_sq - 0.5 * (lam * lam) * dsq;
-        const double gap = primal - dual;
-        int st = ST_OK;
-        if (prev_margin < -1e-9) st = ST_INFEASIBLE;
-        else if (gap < -1e-10) st = ST_NEG_GAP;
-        sc->status = st;
-        sc->gap_pre = gap;
-        sc->radius = sqrt(2.0 * fmax(gap, 0.0)) / lam;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// CD epoch, dense, one CTA per problem (solver.py:82-101, _kernels.py:39-64)
-// ---------------------------------------------------------------------------
-// Thread t owns rows t, t+B, ..., t+(R-1)B of rho in registers.  For each
-// active column in ascending order the CTA either
-//   * skips it: certified zero update (t_i > Delta, see cert_threshold), which
-//     is bit-exact with computing it, or
-//   * computes g = x^T rho (thread FMA chain over its rows, warp butterfly,
-//     warps summed in order), z = beta + g/nsq, u = lam/nsq, soft threshold,
-//     and on d != 0 updates beta and rho -= d*x with separate roundings.
-// Delta (rigorous, round-up) bounds ||rho - rho0|| since the anchor rho0 at
-// which t was computed.  tcert == nullptr disables skipping.
-struct CdArgs {
-    int64_t ld;
-    int n;
-    const int32_t* A;
-    int64_t m;
-    const double* tcert;
-    double* beta;
-    double* rho;
-    const double* nsq;
-    const double* norms;
-    double lam;
-    DevScalars* sc;
-};
-
-__device__ __forceinline__ int64_t cd_next_uncertified(const double* __restrict__ tcert, int64_t pos, int64_t m,
-                                                       double Delta, int* s_first, int& phase) {
-    if (!tcert) return pos;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    while (pos < m) {
-        const int64_t i = pos + threadIdx.x;
-        const bool unc = (i < m) && !(Delta < tcert[i]);
-        const unsigned bal = __ballot_sync(0xffffffffu, unc);
-        int* sf = s_first + phase * 32;
-        if (lane == 0) sf[w] = bal ? (w * 32 + __ffs(bal) - 1) : INT32_MAX;
-        __syncthreads();
-        int f = INT32_MAX;
-        for (int k = 0; k < nw; ++k) f = min(f, sf[k]);
-        phase ^= 1;
-        if (f != INT32_MAX) return pos + f;
-        pos += blockDim.x;
-    }
-    return m;
-}
-
-template <typename T, int R>
-__global__ void __launch_bounds__(R >= 8 ? 512 : 1024) k_cd_epoch_dense(const T* __restrict__ X, CdArgs a) {
-    __shared__ double s_part[2][32];
-    __shared__ int s_first[2 * 32];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5, B = blockDim.x;
-    double rr[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) { const int r = tid + k * B; rr[k] = r < a.n ? a.rho[r] : 0.0; }
-    const double rho0 = a.sc->rho_norm_ub;
-    const double lam = a.lam;
-    double Delta = 0.0;
-    int pbuf = 0, phase = 0;
-    unsigned long long n_unc = 0, n_nz = 0;
-    int64_t pos = 0;
-    while (true) {
-        const int64_t i = cd_next_uncertified(a.tcert, pos, a.m, Delta, s_first, phase);
-        if (i >= a.m) break;
-        const int64_t j = a.A[i];
-        const T* x = X + j * a.ld;
-        double xv[R];
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            const int r = tid + k * B;
-            xv[k] = r < a.n ? to_d(__ldg(x + r)) : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) acc = fma(xv[k], rr[k], acc);
-        // every thread reads beta_j before the barrier; thread 0 writes it after
-        const double bj = a.beta[j];
-        const double nsq = a.nsq[j];
-        acc = warp_sum(acc);
-        if (lane == 0) s_part[pbuf][w] = acc;
-        __syncthreads();
-        double g = 0.0;
-        for (int k = 0; k < nw; ++k) g += s_part[pbuf][k];
-        pbuf ^= 1;
-        const double z = bj + g / nsq;
-        const double u = lam / nsq;
-        const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
-        const double d = nb - bj;
-        ++n_unc;
-        if (d != 0.0) {
-            ++n_nz;
-            if (tid == 0) a.beta[j] = nb;
-#pragma unroll
-            for (int k = 0; k < R; ++k) rr[k] = __dsub_rn(rr[k], __dmul_rn(d, xv[k]));
-            const double step = __dmul_ru(fabs(d), a.norms[j]);
-            Delta = __dadd_ru(Delta, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12),
-                                               __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, Delta), step))));
-        }
-        pos = i + 1;
-    }
-    // write back rho and a rigorous ||rho|| bound for the next anchor
-    __shared__ double red[32];
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-        const int r = tid + k * B;
-        if (r < a.n) { a.rho[r] = rr[k]; s = __dadd_ru(s, __dmul_ru(rr[k], rr[k])); }
-    }
-    s = block_sum_ru(s, red);
-    if (tid == 0) {
-        a.sc->rho_norm_ub = __dsqrt_ru(s);
-        a.sc->visits += (unsigned long long)a.m;
-        a.sc->uncertified += n_unc;
-        a.sc->nonzero += n_nz;
-    }
-    (void)lane;
-}
-
-// CSC: rho in shared memory; every warp computes the same column dot
-// redundantly (lane-strided over the column's entries, butterfly), so d and
-// Delta are known CTA-wide without an extra barrier; warp 0 applies updates.
-__global__ void __launch_bounds__(1024) k_cd_epoch_csc(const double* __restrict__ data,
-                                                       const int32_t* __restrict__ indices,
-                                                       const int64_t* __restrict__ indptr, CdArgs a) {
-    extern __shared__ double s_rho[];
-    __shared__ int s_first[2 * 32];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    for (int r = tid; r < a.n; r += blockDim.x) s_rho[r] = a.rho[r];
-    __syncthreads();
-    const double rho0 = a.sc->rho_norm_ub;
-    const double lam = a.lam;
-    double Delta = 0.0;
-    int phase = 0;
-    unsigned long long n_unc = 0, n_nz = 0;
-    int64_t pos = 0;
-    while (true) {
-        const int64_t i = cd_next_uncertified(a.tcert, pos, a.m, Delta, s_first, phase);
-        if (!a.tcert) __syncthreads();   // order the previous step's rho writes
-        if (i >= a.m) break;
-        const int64_t j = a.A[i];
-        const int64_t lo = indptr[j], hi = indptr[j + 1];
-        const double bj = a.beta[j];
-        const double nsq = a.nsq[j];
-        double acc = 0.0;
-        for (int64_t q = lo + lane; q < hi; q += kWarp) acc = fma(__ldg(data + q), s_rho[__ldg(indices + q)], acc);
-        const double g = warp_sum(acc);
-        const double z = bj + g / nsq;
-        const double u = lam / nsq;
-        const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
-        const double d = nb - bj;
-        ++n_unc;
-        if (d != 0.0) {
-            ++n_nz;
-            __syncthreads();   // d is CTA-uniform: all warps finished reading rho and beta_j
-            if (w == 0) {
-                if (lane == 0) a.beta[j] = nb;
-                for (int64_t q = lo + lane; q < hi; q += kWarp) {
-                    const int32_t r = __ldg(indices + q);
-                    s_rho[r] = __dsub_rn(s_rho[r], __dmul_rn(d, __ldg(data + q)));
-                }
-            }
-            const double step = __dmul_ru(fabs(d), a.norms[j]);
-            Delta = __dadd_ru(Delta, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12),
-                                               __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, Delta), step))));
-        }
-        pos = i + 1;
-    }
-    __syncthreads();
-    __shared__ double red[32];
-    double s = 0.0;
-    for (int r = tid; r < a.n; r += blockDim.x) { const double q = s_rho[r]; a.rho[r] = q; s = __dadd_ru(s, __dmul_ru(q, q)); }
-    s = block_sum_ru(s, red);
-    if (tid == 0) {
-        a.sc->rho_norm_ub = __dsqrt_ru(s);
-        a.sc->visits += (unsigned long long)a.m;
-        a.sc->uncertified += n_unc;
-        a.sc->nonzero += n_nz;
-    }
 }
 
 // ---------------------------------------------------------------------------

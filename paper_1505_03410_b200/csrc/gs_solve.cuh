@@ -1,0 +1,1064 @@
+// Persistent per-problem solve kernel: Algorithm 1 of the paper
+// (solver.py:149-246) as ONE cooperative launch per lambda.
+//
+// A "group" of G co-resident CTAs owns one problem.  Phases that stream the
+// design (residual resync, restricted X^T rho, sequential full-p screen,
+// certification refresh) are split over all G CTAs; the scalar algebra and
+// the serial CD epoch run on CTA 0 while the rest wait at the group barrier.
+// There is no host round trip between checkpoints: the host launches once
+// per lambda (or once per checkpoint when a checkpoint hook needs the active
+// set on the host).
+//
+// Certified-zero skipping (exact): every active position i carries a
+// threshold t_i (gs_kernels.cuh: cert_threshold) computed from an anchor
+// residual rho0; Delta >= ||rho - rho0|| is accumulated rigorously (round-up)
+// over CD updates and checkpoint drop-axpys.  A position with beta == 0 and
+// Delta < t_i provably yields a zero update and is skipped without reading
+// its column.  The anchor is refreshed (one GEMV over X_A by the whole group)
+// only when skipping degrades, and after every residual resync.
+#pragma once
+#include "gs_kernels.cuh"
+
+namespace gs {
+
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+struct GroupBar {
+    unsigned count;
+    unsigned gen;
+};
+
+// loop / control state of one solve, persistent across (hook-mode) launches
+struct SolveCtl {
+    int64_t k, passes, ntrace, nckpt;
+    int32_t started, resume, pending, done, converged, status, need_refresh, final_done;
+    double cd_delta, anchor_norm;
+    int64_t epoch_unc, epoch_nz;
+    int64_t n_refresh;
+    // device-side phase timers (%globaltimer, ns), CTA 0 thread 0
+    unsigned long long t_screen, t_ckpt, t_refresh, t_cd;
+    int64_t n_screen;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+enum Pending : int32_t { PEND_NONE = 0, PEND_CONTINUE = 1, PEND_CONVERGED = 2, PEND_BREAK = 3 };
+
+struct SolveDev {
+    // design
+    const void* X;
+    int64_t ld;
+    int n;
+    int dtype;
+    int64_t p;
+    int sparse;
+    const double* data;
+    const int32_t* indices;
+    const int64_t* indptr;
+    const double* csr_data;
+    const int32_t* csr_cols;
+    const int64_t* csr_rowptr;
+    const double* norms;
+    const double* nsq;
+    // state
+    const double* y;
+    double* beta;
+    double* rho;
+    double* theta;
+    double* c;
+    float* t;
+    float* t2;
+    int32_t* A;
+    int32_t* A2;
+    int32_t* S;
+    int32_t* Dl;
+    uint8_t* mark;
+    double* partial;
+    int nch_max;
+    DevScalars* sc;
+    SolveCtl* ctl;
+    TraceRow* trace;
+    int64_t trace_cap;
+    GroupBar* bar;
+    double* cta_val;     // [G]
+    int64_t* cta_idx;    // [G]
+    int64_t* cta_cnt;    // [2 G]
+    // parameters
+    double lam, eps;
+    int64_t max_passes, f;
+    int rule;            // GS_RULE_*
+    int certify;
+    int stop_at_ckpt;    // hook mode: return to the host after every checkpoint
+    int init_mode;       // 0 all nonzero-norm columns, 1 host list in A2 (count in sc->cnt), 2 sequential screen
+    double prev_margin;
+    int refresh_excess;
+    int cd_warps;        // CD warp-group size
+    int vs_cap;          // max n staged in shared memory for the GEMV
+};
+
+struct Group {
+    int G, c;
+    GroupBar* bar;
+};
+
+__device__ __forceinline__ void group_sync(const Group& g) {
+    __syncthreads();
+    if (g.G > 1) {
+        if (threadIdx.x == 0) {
+            volatile unsigned* genp = &g.bar->gen;
+            const unsigned my = *genp;
+            __threadfence();
+            const unsigned arrived = atomicAdd(&g.bar->count, 1u);
+            if (arrived == (unsigned)g.G - 1u) {
+                atomicExch(&g.bar->count, 0u);
+                __threadfence();
+                atomicAdd(&g.bar->gen, 1u);
+            } else {
+                while (*genp == my) __nanosleep(32);
+            }
+            __threadfence();   // acquire: also invalidates this SM's L1
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// group-wide stable compaction over positions [0, m): each CTA owns one
+// contiguous range, counts, then scatters at its prefix offset.  Two
+// independent predicates are compacted in the same two phases.
+// ---------------------------------------------------------------------------
+template <class PredA, class EmitA, class PredB, class EmitB>
+__device__ void group_compact2(const Group& g, const SolveDev& P, int64_t m, PredA pa, EmitA ea, PredB pb,
+                               EmitB eb, int64_t* total_a, int64_t* total_b, int* sh) {
+    const int64_t per = (m + g.G - 1) / g.G;
+    const int64_t lo = min(m, (int64_t)g.c * per), hi = min(m, lo + per);
+    int ca = 0, cb = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) { ca += pa(i) ? 1 : 0; cb += pb(i) ? 1 : 0; }
+    int tot;
+    block_excl_scan(ca, sh, tot);
+    const int64_t cta_a = tot;
+    block_excl_scan(cb, sh, tot);
+    const int64_t cta_b = tot;
+    if (threadIdx.x == 0) { P.cta_cnt[2 * g.c] = cta_a; P.cta_cnt[2 * g.c + 1] = cta_b; }
+    group_sync(g);
+    int64_t oa = 0, ob = 0, ta = 0, tb = 0;
+    for (int k = 0; k < g.G; ++k) {
+        const int64_t va = P.cta_cnt[2 * k], vb = P.cta_cnt[2 * k + 1];
+        if (k < g.c) { oa += va; ob += vb; }
+        ta += va; tb += vb;
+    }
+    // stable scatter, blockDim positions per round
+    for (int64_t base = lo; base < hi; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const int fa = (i < hi && pa(i)) ? 1 : 0;
+        const int fb = (i < hi && pb(i)) ? 1 : 0;
+        int na, nb;
+        const int ra = block_excl_scan(fa, sh, na);
+        const int rb = block_excl_scan(fb, sh, nb);
+        if (fa) ea(i, oa + ra);
+        if (fb) eb(i, ob + rb);
+        oa += na;
+        ob += nb;
+    }
+    if (g.c == 0 && threadIdx.x == 0) {
+        if (total_a) *total_a = ta;
+        if (total_b) *total_b = tb;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// group GEMV over positions (cols == nullptr: identity), warp per column,
+// columns interleaved over all warps of the group.  v staged in shared memory
+// when it fits.  Emits per-CTA (max |c|, position) into P.cta_val/cta_idx.
+// ---------------------------------------------------------------------------
+enum GMode : int { G_DUAL = 0, G_CERT = 1, G_MU = 2 };
+
+template <typename T>
+__device__ void group_gemv(const Group& g, const SolveDev& P, const double* v, const int32_t* cols, int64_t m,
+                           int mode, double* out_c, float* out_t, double rho0, double gam, double radius,
+                           double* vs) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int n = P.n;
+    const bool stage = n <= P.vs_cap;
+    if (stage) {
+        for (int r = threadIdx.x; r < n + 2; r += blockDim.x) vs[r] = r < n ? v[r] : 0.0;
+        __syncthreads();
+    }
+    const double* vv = stage ? vs : v;
+    double bmax = -1.0;
+    int64_t barg = INT64_MAX;
+    const int64_t GW = (int64_t)g.G * W;
+    // per-column epilogue (lane 0); nrm/bj were loaded before the dot
+    auto epilogue = [&](int64_t i, int64_t j, double cval, double nrm, double bj) {
+        if (mode == G_MU) {
+            const double mu = fabs(cval) + radius * nrm;
+            P.mark[j] = (mu >= 1.0 - 1e-9) && nrm > 0.0;
+        } else {
+            if (out_c) out_c[i] = cval;
+            argmax_merge(bmax, barg, fabs(cval), i);
+            if (mode == G_CERT) {
+                const double tt = (bj != 0.0) ? -1.0 : cert_threshold(cval, nrm, P.lam, rho0, gam);
+                out_t[i] = __double2float_rd(tt);
+            }
+        }
+    };
+    if (P.sparse) {
+        for (int64_t i = (int64_t)g.c * W + w; i < m; i += GW) {
+            const int64_t j = cols ? (int64_t)cols[i] : i;
+            const double nrm = __ldg(P.norms + j);
+            const double bj = (mode == G_CERT) ? P.beta[j] : 0.0;
+            const int64_t lo = __ldg(P.indptr + j), hi = __ldg(P.indptr + j + 1);
+            double acc = 0.0;
+            for (int64_t q = lo + lane; q < hi; q += kWarp) acc = fma(__ldg(P.data + q), vv[__ldg(P.indices + q)], acc);
+            const double cval = warp_sum(acc);
+            if (lane == 0) epilogue(i, j, cval, nrm, bj);
+        }
+    } else {
+        const T* X = (const T*)P.X;
+        // each warp takes two columns (i, i + GW) per round
+        for (int64_t i = (int64_t)g.c * W + w; i < m; i += 2 * GW) {
+            const int64_t i1 = i + GW;
+            const bool two = i1 < m;
+            const int64_t j0 = cols ? (int64_t)cols[i] : i;
+            const int64_t j1 = two ? (cols ? (int64_t)cols[i1] : i1) : j0;
+            const double nrm0 = __ldg(P.norms + j0), nrm1 = __ldg(P.norms + j1);
+            const double bj0 = (mode == G_CERT) ? P.beta[j0] : 0.0;
+            const double bj1 = (mode == G_CERT) ? P.beta[j1] : 0.0;
+            double c0, c1;
+            ColDot2<T>::run(X + j0 * P.ld, X + j1 * P.ld, vv, n, lane, c0, c1);
+            if (lane == 0) {
+                epilogue(i, j0, c0, nrm0, bj0);
+                if (two) epilogue(i1, j1, c1, nrm1, bj1);
+            }
+        }
+    }
+    if (mode != G_MU) {
+        __shared__ double s_v[32];
+        __shared__ int64_t s_i[32];
+        warp_argmax(bmax, barg);
+        if (lane == 0) { s_v[w] = bmax; s_i[w] = barg; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < W; ++k) argmax_merge(bmax, barg, s_v[k], s_i[k]);
+            P.cta_val[g.c] = bmax;
+            P.cta_idx[g.c] = barg;
+        }
+    }
+}
+
+// max over the per-CTA partials (every caller thread gets the same answer)
+__device__ __forceinline__ void group_max_result(const Group& g, const SolveDev& P, double& v, int64_t& i) {
+    v = -1.0;
+    i = INT64_MAX;
+    for (int k = 0; k < g.G; ++k) argmax_merge(v, i, P.cta_val[k], P.cta_idx[k]);
+    if (v < 0.0) { v = 0.0; i = 0; }
+}
+
+// ---------------------------------------------------------------------------
+// residual resync rho = y - X beta over the support (design_matrix.py:130-137)
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ void group_resync(const Group& g, const SolveDev& P, int64_t m, int* sh) {
+    const int n = P.n;
+    // support list S = {A_i : beta_{A_i} != 0}, ascending (l1 norms, dense products)
+    const int32_t* A = P.A;
+    group_compact2(g, P, m,
+                   [&](int64_t i) { return P.beta[A[i]] != 0.0; },
+                   [&](int64_t i, int64_t o) { P.S[o] = A[i]; },
+                   [&](int64_t) { return false; }, [&](int64_t, int64_t) {},
+                   &P.sc->n_supp, nullptr, sh);
+    group_sync(g);
+    if (P.sparse) {
+        for (int64_t r = (int64_t)g.c * blockDim.x + threadIdx.x; r < n; r += (int64_t)g.G * blockDim.x) {
+            double s = 0.0;
+            for (int64_t q = __ldg(P.csr_rowptr + r); q < __ldg(P.csr_rowptr + r + 1); ++q)
+                s = fma(__ldg(P.csr_data + q), P.beta[__ldg(P.csr_cols + q)], s);
+            P.rho[r] = __ldg(P.y + r) - s;
+        }
+        group_sync(g);
+        return;
+    }
+    const int64_t s = P.sc->n_supp;
+    const int B = blockDim.x;
+    const int nrb = (n + B - 1) / B;
+    const int nch = (int)imin64(P.nch_max, imax64(1, (s + 15) / 16));
+    const int64_t per = (s + nch - 1) / nch;
+    const T* X = (const T*)P.X;
+    if (s > 0) {
+        for (int task = g.c; task < nrb * nch; task += g.G) {
+            const int rb = task % nrb, ch = task / nrb;
+            const int r = rb * B + threadIdx.x;
+            if (r < n) {
+                const int64_t k0 = (int64_t)ch * per, k1 = min(s, k0 + per);
+                double acc = 0.0;
+                for (int64_t k = k0; k < k1; ++k) {
+                    const int64_t j = P.S[k];
+                    acc = fma(to_d(__ldg(X + j * P.ld + r)), P.beta[j], acc);
+                }
+                P.partial[(int64_t)ch * n + r] = acc;
+            }
+        }
+    }
+    group_sync(g);
+    for (int64_t r = (int64_t)g.c * B + threadIdx.x; r < n; r += (int64_t)g.G * B) {
+        double sum = 0.0;
+        if (s > 0)
+            for (int ch = 0; ch < nch; ++ch) sum += P.partial[(int64_t)ch * n + r];
+        P.rho[r] = __ldg(P.y + r) - sum;
+    }
+    group_sync(g);
+}
+
+// ---------------------------------------------------------------------------
+// checkpoint scalar algebra on CTA 0 (problem.py:98-123, 57-86; regions.py:213-218)
+// l1 over the support list (beta is zero elsewhere).
+// ---------------------------------------------------------------------------
+__device__ void cta_dual(const SolveDev& P, double corr, int want_radius, bool l1_over_support, int64_t m,
+                         double* red) {
+    DevScalars* sc = P.sc;
+    const double lam = P.lam;
+    const int n = P.n;
+    double a = 0.0, b = 0.0, aru = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const double q = P.rho[r];
+        a = fma(q, q, a);
+        b = fma(__ldg(P.y + r), q, b);
+        aru = __dadd_ru(aru, __dmul_ru(q, q));
+    }
+    const double rho_sq = block_sum(a, red);
+    const double y_rho = block_sum(b, red);
+    const double rho_sq_ru = block_sum_ru(aru, red);
+    double alpha = 0.0, margin = 1.0;
+    int interp = 0;
+    if (rho_sq == 0.0) {
+        interp = 1;
+    } else {
+        const double raw = y_rho / (lam * rho_sq);
+        if (corr > 0.0) {
+            const double bound = 1.0 / corr;
+            alpha = fmin(fmax(raw, -bound), bound);
+        } else {
+            alpha = raw;
+        }
+        margin = 1.0 - fabs(alpha) * corr;
+    }
+    double dd = 0.0, l1 = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const double th = interp ? 0.0 : alpha * P.rho[r];
+        P.theta[r] = th;
+        const double diff = th - __ldg(P.y + r) / lam;
+        dd = fma(diff, diff, dd);
+    }
+    if (l1_over_support) {
+        const int64_t s = sc->n_supp;
+        for (int64_t i = threadIdx.x; i < s; i += blockDim.x) l1 += fabs(P.beta[P.S[i]]);
+    } else {
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) l1 += fabs(P.beta[P.A[i]]);
+    }
+    const double dsq = block_sum(dd, red);
+    const double l1s = block_sum(l1, red);
+    if (threadIdx.x == 0) {
+        const double dual = 0.5 * sc->y_norm_sq - 0.5 * (lam * lam) * dsq;
+        const double primal = 0.5 * rho_sq + lam * l1s;
+        const double gap = primal - dual;
+        sc->rho_sq = rho_sq; sc->y_rho = y_rho; sc->alpha = alpha; sc->margin = margin; sc->interp = interp;
+        sc->corr = corr; sc->l1 = l1s; sc->primal = primal; sc->dual = dual; sc->gap_pre = gap;
+        int st = ST_OK;
+        if (margin < -1e-9) st = ST_INFEASIBLE;
+        else if (want_radius && gap < -1e-10) st = ST_NEG_GAP;
+        sc->status = st;
+        sc->radius = sqrt(2.0 * fmax(gap, 0.0)) / lam;
+        sc->rho_norm_ub = __dsqrt_ru(rho_sq_ru);
+    }
+    __syncthreads();
+}
+
+// post-drop certificate (solver.py:217-221): zero the dropped beta, add the
+// drop-axpy drift to Delta, recompute P with the same theta, trace row.
+__device__ void cta_post(const SolveDev& P, double* red) {
+    DevScalars* sc = P.sc;
+    SolveCtl* ctl = P.ctl;
+    const double lam = P.lam;
+    const int n = P.n;
+    // drift of the drop axpys (before zeroing beta)
+    const int64_t nd = sc->n_drop;
+    double dr = 0.0;
+    for (int64_t k = threadIdx.x; k < nd; k += blockDim.x) {
+        const int32_t j = P.Dl[k];
+        dr = __dadd_ru(dr, __dmul_ru(fabs(P.beta[j]), __ldg(P.norms + j)));
+    }
+    const double drift = block_sum_ru(dr, red);
+    for (int64_t k = threadIdx.x; k < nd; k += blockDim.x) P.beta[P.Dl[k]] = 0.0;
+    __syncthreads();
+    double a = 0.0, aru = 0.0, l1 = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const double q = P.rho[r];
+        a = fma(q, q, a);
+        aru = __dadd_ru(aru, __dmul_ru(q, q));
+    }
+    const int64_t s = sc->n_supp;
+    for (int64_t i = threadIdx.x; i < s; i += blockDim.x) l1 += fabs(P.beta[P.S[i]]);
+    const double rho_sq = block_sum(a, red);
+    const double rho_sq_ru = block_sum_ru(aru, red);
+    const double l1s = block_sum(l1, red);
+    if (threadIdx.x == 0) {
+        const double primal = 0.5 * rho_sq + lam * l1s;
+        const double gap = primal - sc->dual;
+        sc->primal_post = primal;
+        sc->gap_post = gap;
+        sc->radius_post = sqrt(2.0 * fmax(gap, 0.0)) / lam;
+        const double anchor = sc->rho_norm_ub;          // pre-drop rho: the anchor of t
+        ctl->anchor_norm = anchor;
+        // rigorous drift bound of the drop axpys: sum|b_j||x_j| (1+k) + u (||rho0|| + drift)
+        ctl->cd_delta = __dadd_ru(__dmul_ru(drift, 1.0 + 1e-12),
+                                  __dmul_ru(2.3e-16 * (double)imax64(nd, 1), __dadd_ru(anchor, drift)));
+        if (nd == 0) ctl->cd_delta = 0.0;
+        sc->rho_norm_ub = __dsqrt_ru(rho_sq_ru);
+        if (ctl->ntrace < P.trace_cap) P.trace[ctl->ntrace] = TraceRow{ctl->passes, sc->m, gap, sc->radius_post};
+        ctl->ntrace++;
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// CD epoch, dense, run by the first W warps of CTA 0
+// ---------------------------------------------------------------------------
+constexpr int kTTile = 8192;   // certification thresholds staged per tile (float)
+// dense CD shared-memory region: thresholds, active indices, reduction slots
+constexpr int kCdBytes = kTTile * (int)(sizeof(float) + sizeof(int32_t)) + 64 * 8;
+
+__device__ __forceinline__ int64_t scan_tile(const float* ts, int64_t tb, int64_t tend, int64_t from, double D,
+                                             int lane) {
+    for (int64_t base = from; base < tend; base += 32) {
+        const int64_t q = base + lane;
+        const bool unc = q < tend && !(D < (double)ts[q - tb]);
+        const unsigned b = __ballot_sync(0xffffffffu, unc);
+        if (b) return base + __ffs(b) - 1;
+    }
+    return tend;
+}
+
+__device__ __forceinline__ double delta_step(double D, double step, double rho0) {
+    // ||rho_new - rho|| <= |d| ||x|| (1+u) + u ||rho_new||, ||rho_new|| <= rho0 + D + |d| ||x||
+    return __dadd_ru(D, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12), __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, D), step))));
+}
+
+// Software-pipelined serial CD: positions are consumed in ascending order;
+// the next uncertified positions under the current Delta are prefetched two
+// steps ahead (active index from the staged tile, then beta_j, nsq_j, ||x_j||
+// and the thread's rows of x_j into registers).  A nonzero update can only
+// grow Delta, i.e. uncover extra positions before the queued ones; the queue
+// is re-validated with a shared-memory scan and refilled when that happens.
+template <typename T, int R>
+struct CdEnt {
+    int64_t pos;
+    int32_t j;
+    double bj, ns, nr;
+    double x[R];
+};
+
+template <typename T, int R>
+__device__ __forceinline__ void cd_fill(CdEnt<T, R>& e, int64_t pos, int64_t tb, int64_t tend, const int32_t* As,
+                                        const T* __restrict__ X, int64_t ld, int n, const double* beta,
+                                        const double* __restrict__ nsq, const double* __restrict__ norms, int tid,
+                                        int BT) {
+    e.pos = pos;
+    if (pos < tend) {
+        const int32_t j = As[pos - tb];
+        e.j = j;
+        e.bj = beta[j];
+        e.ns = __ldg(nsq + j);
+        e.nr = __ldg(norms + j);
+        const T* x = X + (int64_t)j * ld;
+#pragma unroll
+        for (int k = 0; k < R; ++k) { const int r = tid + k * BT; e.x[k] = r < n ? to_d(__ldg(x + r)) : 0.0; }
+    }
+}
+
+template <typename T, int R>
+__device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m, int W, unsigned char* smem,
+                                            int* tile_valid) {
+    SolveCtl* ctl = P.ctl;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int BT = W * 32;
+    float* ts = reinterpret_cast<float*>(smem);
+    int32_t* As = reinterpret_cast<int32_t*>(smem + kTTile * sizeof(float));
+    double* part = reinterpret_cast<double*>(smem + kTTile * (sizeof(float) + sizeof(int32_t)));   // [2][32]
+    const T* __restrict__ X = (const T*)P.X;
+    const int n = P.n;
+    const int64_t ld = P.ld;
+    const int32_t* Ag = P.A;
+    float* tg = P.t;
+    double* beta = P.beta;
+    const double* __restrict__ nsq = P.nsq;
+    const double* __restrict__ norms = P.norms;
+    if (w < W && m > 0) {
+        double rr[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) { const int r = tid + k * BT; rr[k] = r < n ? P.rho[r] : 0.0; }
+        const bool use_t = P.certify != 0;
+        double D = use_t ? ctl->cd_delta : 0.0;
+        const double rho0 = ctl->anchor_norm;
+        const double lam = P.lam;
+        int64_t tb = 0, tend = 0;
+        int pb = 0;
+        int64_t n_unc = 0, n_nz = 0;
+        auto load_tile = [&](int64_t from) {
+            tb = from;
+            tend = min(m, from + (int64_t)kTTile);
+            if (W > 1) named_bar(1, BT);
+#pragma unroll 4
+            for (int64_t q = tb + tid; q < tend; q += BT) {
+                As[q - tb] = Ag[q];
+                if (use_t) ts[q - tb] = tg[q];
+            }
+            if (W > 1) named_bar(1, BT); else __syncwarp();
+        };
+        auto scan = [&](int64_t from, int64_t lim) -> int64_t {
+            if (from >= lim) return lim;
+            if (!use_t) return from;
+            return scan_tile(ts, tb, lim, from, D, lane);
+        };
+        auto fill = [&](CdEnt<T, R>& e, int64_t pos) { cd_fill<T, R>(e, pos, tb, tend, As, X, ld, n, beta, nsq, norms, tid, BT); };
+        CdEnt<T, R> ea, eb, ec;
+        auto prime = [&](int64_t from, CdEnt<T, R>& e0, CdEnt<T, R>& e1, CdEnt<T, R>& e2) {
+            while (true) {
+                const int64_t p0 = scan(from, tend);
+                if (p0 < tend || tend >= m) { fill(e0, p0); break; }
+                load_tile(tend);
+                from = tb;
+            }
+            fill(e1, scan(e0.pos + 1, tend));
+            fill(e2, scan(e1.pos + 1, tend));
+        };
+        // the tile of (index, threshold) stays resident across epochs while
+        // the active set and thresholds are unchanged and fit one tile
+        if (m <= kTTile && *tile_valid) {
+            tb = 0;
+            tend = m;
+        } else {
+            load_tile(0);
+        }
+        // one step on `cur`; afterwards the ring order is (nxt, nxt2, cur)
+        // with `cur` refilled as the third entry -- no register copies, so a
+        // prefetch issued two steps ahead is consumed two steps later.
+        auto step = [&](CdEnt<T, R>& cur, CdEnt<T, R>& nxt, CdEnt<T, R>& nxt2) -> bool {
+            if (cur.pos >= tend) {
+                if (tend >= m) return false;
+                prime(tend, cur, nxt, nxt2);
+                if (cur.pos >= tend) return false;
+            }
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc = fma(cur.x[k], rr[k], acc);
+            acc = warp_sum(acc);
+            double g;
+            if (W > 1) {
+                if (lane == 0) part[pb * 32 + w] = acc;
+                named_bar(1, BT);
+                g = 0.0;
+                for (int k = 0; k < W; ++k) g += part[pb * 32 + k];
+                pb ^= 1;
+            } else {
+                g = acc;
+            }
+            const double bj = cur.bj;
+            const double z = bj + g / cur.ns;
+            const double u = lam / cur.ns;
+            const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+            const double d = nb - bj;
+            ++n_unc;
+            if (d != 0.0) {
+                ++n_nz;
+                if (tid == 0) {
+                    beta[cur.j] = nb;
+                    if (use_t && bj == 0.0) tg[cur.pos] = -1.0f;   // now in the support
+                }
+                if (use_t && bj == 0.0) ts[cur.pos - tb] = -1.0f;  // (same value in every CD thread)
+#pragma unroll
+                for (int k = 0; k < R; ++k) rr[k] = __dsub_rn(rr[k], __dmul_rn(d, cur.x[k]));
+                if (use_t) {
+                    D = delta_step(D, __dmul_ru(fabs(d), cur.nr), rho0);
+                    // Delta grew: positions before the queued ones may now be uncertified
+                    const int64_t n1 = scan(cur.pos + 1, nxt.pos);
+                    if (n1 != nxt.pos) {
+                        fill(nxt, n1);
+                        fill(nxt2, scan(n1 + 1, tend));
+                        fill(cur, scan(nxt2.pos + 1, tend));
+                        return true;
+                    }
+                    if (nxt.pos < tend) {
+                        const int64_t n2 = scan(nxt.pos + 1, nxt2.pos);
+                        if (n2 != nxt2.pos) fill(nxt2, n2);
+                    }
+                }
+            }
+            fill(cur, scan(nxt2.pos + 1, tend));
+            return true;
+        };
+        prime(0, ea, eb, ec);
+        while (step(ea, eb, ec) && step(eb, ec, ea) && step(ec, ea, eb)) {
+        }
+        if (W > 1) named_bar(1, BT);
+        // write back rho, ||rho|| bound (next anchor), Delta, counters
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int r = tid + k * BT;
+            if (r < n) { P.rho[r] = rr[k]; s = __dadd_ru(s, __dmul_ru(rr[k], rr[k])); }
+        }
+        s = warp_sum_ru(s);
+        if (W > 1) {
+            if (lane == 0) part[pb * 32 + w] = s;
+            named_bar(1, BT);
+            double tot = 0.0;
+            for (int k = 0; k < W; ++k) tot = __dadd_ru(tot, part[pb * 32 + k]);
+            s = tot;
+        }
+        if (tid == 0) {
+            P.sc->rho_norm_ub = __dsqrt_ru(s);
+            ctl->cd_delta = D;
+            ctl->epoch_unc = n_unc;
+            ctl->epoch_nz = n_nz;
+            P.sc->visits += (unsigned long long)m;
+            P.sc->uncertified += (unsigned long long)n_unc;
+            P.sc->nonzero += (unsigned long long)n_nz;
+            *tile_valid = (m <= kTTile) ? 1 : 0;
+        }
+    } else if (tid == 0 && m == 0) {
+        ctl->epoch_unc = 0;
+        ctl->epoch_nz = 0;
+    }
+    __syncthreads();
+}
+
+// CSC: one warp, rho in shared memory after the threshold tile.
+__device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m, unsigned char* smem) {
+    SolveCtl* ctl = P.ctl;
+    const int tid = threadIdx.x, lane = tid & 31;
+    float* ts = reinterpret_cast<float*>(smem);
+    double* srho = reinterpret_cast<double*>(smem + kTTile * sizeof(float));
+    const int n = P.n;
+    for (int r = tid; r < n; r += blockDim.x) srho[r] = P.rho[r];
+    __syncthreads();
+    if (tid < 32 && m > 0) {
+        const bool use_t = P.certify != 0;
+        double D = use_t ? ctl->cd_delta : 0.0;
+        const double rho0 = ctl->anchor_norm;
+        const double lam = P.lam;
+        int64_t tb = 0, tend = 0, n_unc = 0, n_nz = 0;
+        auto load_tile = [&](int64_t from) {
+            tb = from;
+            tend = min(m, from + (int64_t)kTTile);
+            if (use_t) {
+                for (int64_t q = tb + lane; q < tend; q += 32) ts[q - tb] = P.t[q];
+                __syncwarp();
+            }
+        };
+        auto scan = [&](int64_t from) -> int64_t {
+            if (!use_t) return from < tend ? from : tend;
+            return scan_tile(ts, tb, tend, from, D, lane);
+        };
+        load_tile(0);
+        int64_t i = scan(0);
+        while (true) {
+            while (i == tend && tend < m) { load_tile(tend); i = scan(tb); }
+            if (i >= m) break;
+            const int32_t j = P.A[i];
+            const double bj = P.beta[j];
+            const double ns = __ldg(P.nsq + j);
+            const int64_t lo = __ldg(P.indptr + j), hi = __ldg(P.indptr + j + 1);
+            double acc = 0.0;
+            for (int64_t q = lo + lane; q < hi; q += 32) acc = fma(__ldg(P.data + q), srho[__ldg(P.indices + q)], acc);
+            const double g = warp_sum(acc);
+            const double z = bj + g / ns;
+            const double u = lam / ns;
+            const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+            const double d = nb - bj;
+            ++n_unc;
+            if (d != 0.0) {
+                ++n_nz;
+                if (lane == 0) {
+                    P.beta[j] = nb;
+                    if (use_t && bj == 0.0) P.t[i] = -1.0f;
+                }
+                for (int64_t q = lo + lane; q < hi; q += 32) {
+                    const int32_t r = __ldg(P.indices + q);
+                    srho[r] = __dsub_rn(srho[r], __dmul_rn(d, __ldg(P.data + q)));
+                }
+                __syncwarp();
+                if (use_t) D = delta_step(D, __dmul_ru(fabs(d), __ldg(P.norms + j)), rho0);
+            }
+            i = scan(i + 1);
+        }
+        if (lane == 0) {
+            ctl->cd_delta = D;
+            ctl->epoch_unc = n_unc;
+            ctl->epoch_nz = n_nz;
+            P.sc->visits += (unsigned long long)m;
+            P.sc->uncertified += (unsigned long long)n_unc;
+            P.sc->nonzero += (unsigned long long)n_nz;
+        }
+    } else if (tid == 0 && m == 0) {
+        ctl->epoch_unc = 0;
+        ctl->epoch_nz = 0;
+    }
+    __syncthreads();
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int r = tid; r < n; r += blockDim.x) { const double q = srho[r]; P.rho[r] = q; s = __dadd_ru(s, __dmul_ru(q, q)); }
+    s = block_sum_ru(s, red);
+    if (tid == 0) P.sc->rho_norm_ub = __dsqrt_ru(s);
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// the persistent solve kernel
+// ---------------------------------------------------------------------------
+template <typename T, int R>
+__device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* smem) {
+    __shared__ int sh[32];
+    __shared__ double red[32];
+    DevScalars* sc = P.sc;
+    SolveCtl* ctl = P.ctl;
+    // dense: [CD tile | vs]; sparse: the CD uses [t tile | rho] and vs aliases it
+    double* vs = reinterpret_cast<double*>(smem + (P.sparse ? 0 : kCdBytes));
+    __shared__ int s_tile_valid;
+    if (threadIdx.x == 0) s_tile_valid = 0;
+    __syncthreads();
+    const bool gap_rule = P.rule == 1;
+    const double gam = gamma_n(P.sparse ? (int64_t)P.n : (int64_t)P.n);
+
+    if (ctl->done) return;
+
+    // ---- init: active set, beta zeroed outside it (solver.py:163-178) ----
+    if (!ctl->started) {
+        if (P.init_mode == 2) {
+            // sequential gap-sphere screen (path.py:82-91): gap at the new lambda
+            // for the previous (beta, theta, rho), then the fused full-p test.
+            if (g.c == 0) {
+                const double lam = P.lam;
+                double a = 0.0, dd = 0.0, l1 = 0.0;
+                for (int r = threadIdx.x; r < P.n; r += blockDim.x) {
+                    const double q = P.rho[r];
+                    a = fma(q, q, a);
+                    const double diff = P.theta[r] - __ldg(P.y + r) / lam;
+                    dd = fma(diff, diff, dd);
+                }
+                const int64_t m0 = sc->m;
+                for (int64_t i = threadIdx.x; i < m0; i += blockDim.x) l1 += fabs(P.beta[P.A[i]]);
+                const double rho_sq = block_sum(a, red), dsq = block_sum(dd, red), l1s = block_sum(l1, red);
+                if (threadIdx.x == 0) {
+                    const double primal = 0.5 * rho_sq + lam * l1s;
+                    const double dual = 0.5 * sc->y_norm_sq - 0.5 * (lam * lam) * dsq;
+                    const double gap = primal - dual;
+                    int st = ST_OK;
+                    if (P.prev_margin < -1e-9) st = ST_INFEASIBLE;
+                    else if (gap < -1e-10) st = ST_NEG_GAP;
+                    sc->status = st;
+                    sc->gap_pre = gap;
+                    sc->radius = sqrt(2.0 * fmax(gap, 0.0)) / lam;
+                }
+            }
+            group_sync(g);
+            if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
+            const unsigned long long ts0 = gtimer();
+            group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, gam, sc->radius, vs);
+            group_sync(g);
+            if (g.c == 0 && threadIdx.x == 0) { ctl->t_screen += gtimer() - ts0; ctl->n_screen++; }
+        } else if (P.init_mode == 0) {
+            for (int64_t j = (int64_t)g.c * blockDim.x + threadIdx.x; j < P.p; j += (int64_t)g.G * blockDim.x)
+                P.mark[j] = __ldg(P.norms + j) > 0.0;
+            group_sync(g);
+        } else {
+            const int64_t n0 = sc->cnt;
+            for (int64_t i = (int64_t)g.c * blockDim.x + threadIdx.x; i < n0; i += (int64_t)g.G * blockDim.x) {
+                const int32_t j = P.A2[i];
+                if (__ldg(P.norms + j) > 0.0) P.mark[j] = 1;
+            }
+            group_sync(g);
+        }
+        // A = {j : mark_j}; beta_j = 0 off A; mark cleared
+        group_compact2(g, P, P.p,
+                       [&](int64_t j) { return P.mark[j] != 0; },
+                       [&](int64_t j, int64_t o) { P.A[o] = (int32_t)j; },
+                       [&](int64_t) { return false; }, [&](int64_t, int64_t) {},
+                       &sc->m, nullptr, sh);
+        group_sync(g);
+        for (int64_t j = (int64_t)g.c * blockDim.x + threadIdx.x; j < P.p; j += (int64_t)g.G * blockDim.x) {
+            if (!P.mark[j]) P.beta[j] = 0.0;
+            P.mark[j] = 0;
+        }
+        if (g.c == 0 && threadIdx.x == 0) {
+            ctl->started = 1;
+            ctl->k = 1;
+            ctl->passes = 0;
+            ctl->ntrace = 0;
+            ctl->nckpt = 0;
+            ctl->resume = 0;
+            ctl->pending = PEND_NONE;
+            ctl->converged = 0;
+            ctl->need_refresh = 1;
+            ctl->cd_delta = 0.0;
+        }
+        group_sync(g);
+    }
+
+    int64_t k = ctl->k;
+    int32_t pending = ctl->pending;
+    bool broke = false, converged = false;
+    if (pending == PEND_CONVERGED) { converged = true; k = P.max_passes + 1; }
+    else if (pending == PEND_BREAK) { broke = true; k = P.max_passes + 1; }
+
+    while (k <= P.max_passes) {
+        const bool ckpt_pass = (P.f == 1 || k % P.f == 1);
+        const bool is_ckpt = ckpt_pass && pending != PEND_CONTINUE;
+        pending = PEND_NONE;
+        if (is_ckpt) {
+            const unsigned long long tc0 = gtimer();
+            int64_t m = sc->m;
+            group_resync<T>(g, P, m, sh);
+            if (m == 0) {
+                // everything screened: unrestricted dual point (solver.py:190-203)
+                group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs);
+                group_sync(g);
+                if (g.c == 0) {
+                    double corr; int64_t ci;
+                    group_max_result(g, P, corr, ci);
+                    cta_dual(P, corr, 0, true, 0, red);
+                    if (threadIdx.x == 0) {
+                        sc->n_drop = 0;
+                        sc->gap_post = sc->gap_pre;
+                        sc->primal_post = sc->primal;
+                        sc->radius_post = sqrt(2.0 * fmax(sc->gap_pre, 0.0)) / P.lam;
+                        if (ctl->ntrace < P.trace_cap) P.trace[ctl->ntrace] = TraceRow{ctl->passes, 0, sc->gap_pre, sc->radius_post};
+                        ctl->ntrace++;
+                        ctl->nckpt++;
+                        ctl->pending = sc->gap_pre <= P.eps ? PEND_CONVERGED : PEND_BREAK;
+                        ctl->k = k;
+                    }
+                }
+                group_sync(g);
+                if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
+            } else {
+                // restricted |X_A^T rho|_inf with the dots kept for mu and the anchor
+                group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, P.c, nullptr, 0.0, gam, 0.0, vs);
+                group_sync(g);
+                if (g.c == 0) {
+                    double corr; int64_t ci;
+                    group_max_result(g, P, corr, ci);
+                    cta_dual(P, corr, gap_rule ? 1 : 0, true, m, red);
+                }
+                group_sync(g);
+                if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
+                const double alpha = sc->alpha, radius = sc->radius, anchor = sc->rho_norm_ub;
+                const bool cert = P.certify != 0;
+                if (gap_rule) {
+                    // keep = mu >= 1 - 1e-9 with mu = |alpha c| + r ||x|| (solver.py:208-216);
+                    // kept positions carry their certification thresholds along.
+                    const int32_t* A = P.A;
+                    group_compact2(g, P, m,
+                                   [&](int64_t i) {
+                                       const double mu = fabs(alpha * P.c[i]) + radius * __ldg(P.norms + A[i]);
+                                       return mu >= 1.0 - 1e-9;
+                                   },
+                                   [&](int64_t i, int64_t o) {
+                                       const int32_t j = A[i];
+                                       P.A2[o] = j;
+                                       if (cert) {
+                                           const double tt = (P.beta[j] != 0.0) ? -1.0 : cert_threshold(P.c[i], __ldg(P.norms + j), P.lam, anchor, gam);
+                                           P.t2[o] = __double2float_rd(tt);
+                                       }
+                                   },
+                                   [&](int64_t i) {
+                                       const double mu = fabs(alpha * P.c[i]) + radius * __ldg(P.norms + A[i]);
+                                       return !(mu >= 1.0 - 1e-9) && P.beta[A[i]] != 0.0;
+                                   },
+                                   [&](int64_t i, int64_t o) { P.Dl[o] = A[i]; },
+                                   &sc->m, &sc->n_drop, sh);
+                    group_sync(g);
+                    // drop axpys rho += beta_j x_j, ascending j (numpy order per element)
+                    const int64_t nd = sc->n_drop;
+                    if (nd > 0) {
+                        if (P.sparse) {
+                            if (g.c == 0) {
+                                for (int64_t q0 = 0; q0 < nd; ++q0) {
+                                    const int32_t j = P.Dl[q0];
+                                    const double bj = P.beta[j];
+                                    for (int64_t q = __ldg(P.indptr + j) + threadIdx.x; q < __ldg(P.indptr + j + 1); q += blockDim.x) {
+                                        const int32_t r = __ldg(P.indices + q);
+                                        P.rho[r] = __dadd_rn(P.rho[r], __dmul_rn(bj, __ldg(P.data + q)));
+                                    }
+                                    __syncthreads();
+                                }
+                            }
+                        } else {
+                            const T* X = (const T*)P.X;
+                            for (int64_t r = (int64_t)g.c * blockDim.x + threadIdx.x; r < P.n; r += (int64_t)g.G * blockDim.x) {
+                                double q = P.rho[r];
+                                for (int64_t q0 = 0; q0 < nd; ++q0) {
+                                    const int64_t j = P.Dl[q0];
+                                    q = __dadd_rn(q, __dmul_rn(P.beta[j], to_d(__ldg(X + j * P.ld + r))));
+                                }
+                                P.rho[r] = q;
+                            }
+                        }
+                    }
+                    group_sync(g);
+                    if (g.c == 0) {
+                        cta_post(P, red);
+                        if (threadIdx.x == 0) { ctl->need_refresh = cert ? 0 : 1; }
+                    }
+                } else {
+                    // rule none: no drop; thresholds for all positions at this anchor
+                    if (cert) {
+                        for (int64_t i = (int64_t)g.c * blockDim.x + threadIdx.x; i < m; i += (int64_t)g.G * blockDim.x) {
+                            const int32_t j = P.A[i];
+                            const double tt = (P.beta[j] != 0.0) ? -1.0 : cert_threshold(P.c[i], __ldg(P.norms + j), P.lam, anchor, gam);
+                            P.t[i] = __double2float_rd(tt);
+                        }
+                    }
+                    if (g.c == 0 && threadIdx.x == 0) { sc->m = m; sc->n_drop = 0; }
+                    group_sync(g);
+                    if (g.c == 0) {
+                        cta_post(P, red);
+                        if (threadIdx.x == 0) ctl->need_refresh = 0;
+                    }
+                }
+                if (g.c == 0 && threadIdx.x == 0) {
+                    ctl->nckpt++;
+                    const int64_t mn = sc->m;
+                    ctl->pending = sc->gap_post <= P.eps ? PEND_CONVERGED : (mn == 0 ? PEND_BREAK : PEND_CONTINUE);
+                    ctl->k = k;
+                }
+                group_sync(g);
+                if (gap_rule) {
+                    // swap A/A2 and t/t2 (device pointers are per launch; the host swaps between launches)
+                    // handled by copying back: the compaction wrote the new active set into A2/t2
+                    const int64_t mn = sc->m;
+                    for (int64_t i = (int64_t)g.c * blockDim.x + threadIdx.x; i < mn; i += (int64_t)g.G * blockDim.x) {
+                        P.A[i] = P.A2[i];
+                        if (cert) P.t[i] = P.t2[i];
+                    }
+                    group_sync(g);
+                }
+            }
+            if (g.c == 0 && threadIdx.x == 0) { ctl->t_ckpt += gtimer() - tc0; s_tile_valid = 0; }
+            pending = ctl->pending;
+            if (P.stop_at_ckpt) {
+                if (g.c == 0 && threadIdx.x == 0) { ctl->k = k; }
+                return;   // host fires the checkpoint hook, then relaunches
+            }
+            if (pending == PEND_CONVERGED) { converged = true; break; }
+            if (pending == PEND_BREAK) { broke = true; break; }
+            pending = PEND_NONE;
+        } else if (!ckpt_pass && k % 100 == 0) {
+            group_resync<T>(g, P, sc->m, sh);
+            if (g.c == 0) {
+                double a = 0.0;
+                for (int r = threadIdx.x; r < P.n; r += blockDim.x) { const double q = P.rho[r]; a = __dadd_ru(a, __dmul_ru(q, q)); }
+                const double s = block_sum_ru(a, red);
+                if (threadIdx.x == 0) { sc->rho_norm_ub = __dsqrt_ru(s); ctl->need_refresh = 1; }
+            }
+            group_sync(g);
+        }
+        // ---- one CD epoch over the active set ----
+        const int64_t m = sc->m;
+        if (P.certify && ctl->need_refresh && m > 0) {
+            const unsigned long long tr0 = gtimer();
+            const double anchor = sc->rho_norm_ub;
+            group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0, vs);
+            if (g.c == 0 && threadIdx.x == 0) { ctl->anchor_norm = anchor; ctl->cd_delta = 0.0; ctl->n_refresh++; s_tile_valid = 0; }
+            group_sync(g);
+            if (g.c == 0 && threadIdx.x == 0) ctl->t_refresh += gtimer() - tr0;
+        }
+        if (g.c == 0) {
+            const unsigned long long td0 = gtimer();
+            if (P.sparse) cd_epoch_csc(P, m, smem);
+            else cd_epoch_dense<T, R>(P, m, P.cd_warps, smem, &s_tile_valid);
+            if (threadIdx.x == 0) {
+                ctl->t_cd += gtimer() - td0;
+                ctl->passes++;
+                ctl->need_refresh = (ctl->epoch_unc - ctl->epoch_nz > P.refresh_excess) ? 1 : 0;
+            }
+        }
+        group_sync(g);
+        ++k;
+    }
+    // ---- budget exhausted or early break: certify the final iterate (solver.py:237-245)
+    if (!converged) {
+        const int64_t m = sc->m;
+        group_resync<T>(g, P, m, sh);
+        if (m > 0) group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs);
+        else group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs);
+        group_sync(g);
+        if (g.c == 0) {
+            double corr; int64_t ci;
+            group_max_result(g, P, corr, ci);
+            cta_dual(P, corr, 0, true, m, red);
+            if (threadIdx.x == 0) {
+                ctl->converged = sc->gap_pre <= P.eps;
+                ctl->final_done = 1;
+            }
+        }
+    } else if (g.c == 0 && threadIdx.x == 0) {
+        ctl->converged = 1;
+    }
+    if (g.c == 0 && threadIdx.x == 0) { ctl->done = 1; ctl->k = k; }
+    (void)broke;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(256, 1) k_solve(const SolveDev* __restrict__ probs, int G) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x / G;
+    const SolveDev& P = probs[prob];
+    Group g{G, (int)(blockIdx.x % G), P.bar};
+    solve_body<T, R>(P, g, smem);
+}
+
+// gs_cd_pass production twin: anchor at the incoming rho, one refresh, one
+// certified CD epoch (single CTA).
+template <typename T, int R>
+__global__ void __launch_bounds__(256, 1) k_cd_pass_prod(const SolveDev* __restrict__ probs) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double red[32];
+    const SolveDev& P = probs[0];
+    Group g{1, 0, nullptr};
+    const int64_t m = P.sc->m;
+    double a = 0.0;
+    for (int r = threadIdx.x; r < P.n; r += blockDim.x) { const double q = P.rho[r]; a = __dadd_ru(a, __dmul_ru(q, q)); }
+    const double anchor = __dsqrt_ru(block_sum_ru(a, red));
+    const double gam = gamma_n(P.n);
+    if (P.certify) group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0,
+                                 reinterpret_cast<double*>(smem + (P.sparse ? 0 : kCdBytes)));
+    if (threadIdx.x == 0) { P.ctl->anchor_norm = anchor; P.ctl->cd_delta = 0.0; }
+    __syncthreads();
+    __shared__ int s_tile_valid;
+    if (threadIdx.x == 0) s_tile_valid = 0;
+    __syncthreads();
+    if (P.sparse) cd_epoch_csc(P, m, smem);
+    else cd_epoch_dense<T, R>(P, m, P.cd_warps, smem, &s_tile_valid);
+}
+
+// standalone full-p screening pass (the same group_gemv G_MU code the
+// persistent kernel runs for the sequential screen); P.theta = center.
+template <typename T>
+__global__ void __launch_bounds__(256, 1) k_screen_full(const SolveDev* __restrict__ probs, double radius) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SolveDev& P = probs[0];
+    Group g{(int)gridDim.x, (int)blockIdx.x, nullptr};
+    group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, 0.0, radius,
+                  reinterpret_cast<double*>(smem));
+}
+
+}  // namespace gs

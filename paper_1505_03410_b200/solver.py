@@ -206,7 +206,10 @@ class DeviceSolver:
                             active_history=history)
         state.stats = dict(cd_visits=int(res.cd_visits), cd_uncertified=int(res.cd_uncertified),
                            cd_nonzero=int(res.cd_nonzero), checkpoints=int(res.checkpoints),
-                           device_ms=float(res.device_ms))
+                           device_ms=float(res.device_ms), screen_ms=float(res.screen_ms),
+                           ckpt_ms=float(res.ckpt_ms), refresh_ms=float(res.refresh_ms),
+                           cd_ms=float(res.cd_ms), n_screen=int(res.n_screen),
+                           n_refresh=int(res.n_refresh), launches=int(res.launches))
         return beta, cert, state
 
 
@@ -235,3 +238,56 @@ def solve(prob: LassoProblem, config: SolverConfig, warm_beta: np.ndarray | None
     if active0 is None:
         return dev.solve(prob.lam, config)
     return dev.solve(prob.lam, config, active0=active0, active0_mode=1)
+
+
+class PathTimer:
+    """Device-side timing for benchmarks: CUDA events on the solver's stream,
+    the standalone full-p screening pass, and the end-to-end path through the
+    public API from pinned host buffers."""
+
+    def __init__(self, dev: DeviceSolver):
+        self.dev = dev
+
+    def start(self) -> None:
+        _lib.check(self.dev._lib.gs_solver_timer(self.dev._h, 0, None))
+
+    def stop_ms(self) -> float:
+        ms = ctypes.c_double()
+        _lib.check(self.dev._lib.gs_solver_timer(self.dev._h, 1, ctypes.byref(ms)))
+        return ms.value
+
+    @staticmethod
+    def screen_pass_ms(X, center: np.ndarray, radius: float, reps: int = 10) -> float:
+        c = np.ascontiguousarray(center, dtype=np.float64)
+        ms = ctypes.c_double()
+        cnt = ctypes.c_int64()
+        _lib.check(X._lib.gs_screen_timed(X.handle, _lib.f64p(c), float(radius), int(reps),
+                                          ctypes.byref(ms), ctypes.byref(cnt)))
+        return ms.value
+
+    @staticmethod
+    def e2e_path_ms(case, grid, config, reps: int = 1):
+        """Wall time of DesignMatrix(host X) + DeviceSolver(host y) + run_path
+        (coefficients back to host), X and y in pinned host memory."""
+        import time as _time
+        from .design_matrix import DesignMatrix
+        from .path import run_path
+        Xh = case.X
+        px = _lib.PinnedArray(Xh.shape[::-1], dtype=Xh.dtype)     # (p, n) C-order == (n, p) F-order
+        px.array[...] = Xh.T
+        py = _lib.PinnedArray(case.y.shape)
+        py.array[...] = case.y
+        Xf = px.array.T
+        best = None
+        for _ in range(reps):
+            t0 = _time.perf_counter()
+            X = DesignMatrix(Xf)
+            dev = DeviceSolver(X, py.array)
+            res = run_path(X, py.array, grid, config, solver=dev)
+            dt = (_time.perf_counter() - t0) * 1e3
+            best = dt if best is None else min(best, dt)
+            del dev, X
+        h2d = Xh.nbytes + case.y.nbytes
+        d2h = res.betas.nbytes + sum(s.residual.nbytes + s.theta.theta.nbytes + s.active.nbytes
+                                     for s in res.states)
+        return best, int(h2d), int(d2h)

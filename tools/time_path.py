@@ -28,5 +28,7 @@ out = dict(config=name, upload_s=t1 - t0, path_s_first=t2 - t1, path_s=t3 - t2,
            cd_uncertified=int(sum(x["cd_uncertified"] for x in st)),
            cd_nonzero=int(sum(x["cd_nonzero"] for x in st)),
            device_ms=float(sum(x["device_ms"] for x in st)),
+           phase_ms={k: float(sum(x[k] for x in st)) for k in ("screen_ms", "ckpt_ms", "refresh_ms", "cd_ms")},
+           refreshes=int(sum(x["n_refresh"] for x in st)),
            converged=int(res.converged.sum()))
 print(json.dumps(out))
