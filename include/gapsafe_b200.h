@@ -149,9 +149,10 @@ void gs_solver_free(gs_solver *S);
 /* CUDA events on the solver's stream: op 0 records the start, op 1 records the
  * stop, synchronizes and returns the elapsed milliseconds in *ms. */
 int gs_solver_timer(gs_solver *S, int op, double *ms);
-/* The full-p sphere screening pass (fused GEMV + test, then stable compaction)
- * launched `reps` times on the matrix stream, timed with CUDA events; *ms is the
- * average per pass, *n_active the survivors of the last pass. */
+/* The full-p sphere screening pass: one warm-up pass (fused GEMV + test, then
+ * stable compaction), then the fused GEMV+test kernel launched `reps` times on
+ * the matrix stream and timed with CUDA events; *ms is the average per launch,
+ * *n_active the survivors. */
 int gs_screen_timed(const gs_matrix *M, const double *center, double radius, int reps, double *ms,
                     int64_t *n_active);
 /* pinned (page-locked) host memory for H2D/D2H at full PCIe rate */

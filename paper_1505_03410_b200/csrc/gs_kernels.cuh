@@ -108,7 +108,7 @@ template <> struct ColDot2<double> {
         const double2* v2 = reinterpret_cast<const double2*>(v);
         const int n2 = n >> 1;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-#pragma unroll 4
+#pragma unroll 8
         for (int q = lane; q < n2; q += kWarp) {
             const double2 xa = __ldg(p0 + q);
             const double2 xb = __ldg(p1 + q);
@@ -669,11 +669,12 @@ __global__ void __launch_bounds__(256) k_col_norms_sq_csc(const double* __restri
 }
 
 __global__ void k_sqrt_vec(const double* __restrict__ a, double add, int64_t p, double* __restrict__ out_sq,
-                           double* __restrict__ out) {
+                           double* __restrict__ out, double* __restrict__ out_inv) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
         const double s = a[j] + add;
         out_sq[j] = s;
         out[j] = sqrt(s);
+        if (out_inv) out_inv[j] = s > 0.0 ? 1.0 / s : 0.0;
     }
 }
 

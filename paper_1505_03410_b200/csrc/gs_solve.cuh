@@ -24,6 +24,10 @@ namespace gs {
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 
+struct alignas(16) ColInfo {        // per column, rebuilt per lambda (u), beta kept current
+    double ns, inv, nr, u, beta, pad;
+};
+
 struct GroupBar {
     unsigned count;
     unsigned gen;
@@ -33,7 +37,8 @@ struct GroupBar {
 struct SolveCtl {
     int64_t k, passes, ntrace, nckpt;
     int32_t started, resume, pending, done, converged, status, need_refresh, final_done;
-    double cd_delta, anchor_norm;
+    double cd_delta, anchor_norm, cd_gstep;
+    int64_t n_requeue;
     int64_t epoch_unc, epoch_nz;
     int64_t n_refresh;
     // device-side phase timers (%globaltimer, ns), CTA 0 thread 0
@@ -65,11 +70,13 @@ struct SolveDev {
     const int64_t* csr_rowptr;
     const double* norms;
     const double* nsq;
+    const double* inv_nsq;   // RN(1/nsq), 0 for empty columns
     // state
     const double* y;
     double* beta;
     double* rho;
     double* theta;
+    struct ColInfo* cinfo;   // per column (nsq, 1/nsq, ||x||, lam/nsq, beta), rebuilt per lambda
     double* c;
     float* t;
     float* t2;
@@ -98,6 +105,7 @@ struct SolveDev {
     double prev_margin;
     int refresh_excess;
     int cd_warps;        // CD warp-group size
+    int cd_bytes;        // dense CD shared-memory region (tile + ring), GEMV staging after it
     int vs_cap;          // max n staged in shared memory for the GEMV
 };
 
@@ -119,7 +127,11 @@ __device__ __forceinline__ void group_sync(const Group& g) {
                 __threadfence();
                 atomicAdd(&g.bar->gen, 1u);
             } else {
-                while (*genp == my) __nanosleep(32);
+                const unsigned long long t0 = gtimer();
+                while (*genp == my) {
+                    __nanosleep(32);
+                    if (gtimer() - t0 > 60000000000ull) __trap();   // never hang the GPU
+                }
             }
             __threadfence();   // acquire: also invalidates this SM's L1
         }
@@ -433,8 +445,6 @@ __device__ void cta_post(const SolveDev& P, double* red) {
 // CD epoch, dense, run by the first W warps of CTA 0
 // ---------------------------------------------------------------------------
 constexpr int kTTile = 8192;   // certification thresholds staged per tile (float)
-// dense CD shared-memory region: thresholds, active indices, reduction slots
-constexpr int kCdBytes = kTTile * (int)(sizeof(float) + sizeof(int32_t)) + 64 * 8;
 
 __device__ __forceinline__ int64_t scan_tile(const float* ts, int64_t tb, int64_t tend, int64_t from, double D,
                                              int lane) {
@@ -452,191 +462,357 @@ __device__ __forceinline__ double delta_step(double D, double step, double rho0)
     return __dadd_ru(D, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12), __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, D), step))));
 }
 
-// Software-pipelined serial CD: positions are consumed in ascending order;
-// the next uncertified positions under the current Delta are prefetched two
-// steps ahead (active index from the staged tile, then beta_j, nsq_j, ||x_j||
-// and the thread's rows of x_j into registers).  A nonzero update can only
-// grow Delta, i.e. uncover extra positions before the queued ones; the queue
-// is re-validated with a shared-memory scan and refilled when that happens.
-template <typename T, int R>
-struct CdEnt {
-    int64_t pos;
+// Serial CD chain, warp-specialized.
+//
+//   producer warp (warp W):  scans the staged thresholds for the next
+//     candidates -- positions uncertified under a pessimistic drift bound
+//     Dp = Delta_published + margin -- and for each one issues two TMA bulk
+//     copies (cp.async.bulk, mbarrier complete_tx) into a ring slot: the
+//     column x_j (contiguous, ld*sizeof(T) bytes) and its packed ColInfo
+//     (nsq, 1/nsq, ||x||, u = lam/nsq, beta).  It then writes the slot header
+//     (position, threshold, Dp, generation), waits for the bytes in order and
+//     publishes ready[slot].
+//   compute warps (0..W-1):  poll ready[slot]; skip candidates certified under
+//     the current Delta; otherwise run the chain  dot -> butterfly [-> cross-
+//     warp sum] -> RN(g/nsq) (RN(1/nsq) + Markstein) -> soft threshold -> axpy,
+//     then publish Delta.  If Delta outgrew an entry's Dp, the positions between
+//     candidates may no longer be certified: they request a restart at the
+//     last processed position + 1 with a new generation and drain stale entries.
+// Candidates are consumed strictly in ascending position order, so the
+// arithmetic is exactly the sequential CD over the uncertified positions.
+constexpr int kRingMax = 16;
+
+
+struct alignas(16) SlotHdr {
+    ColInfo ci;                      // TMA destination (48 B)
+    double tcert;                    // certification threshold of the candidate
+    double dp;                       // pessimistic Delta it was selected under
+    int32_t pos;                     // candidate position; == m: end of epoch
     int32_t j;
-    double bj, ns, nr;
-    double x[R];
+    int32_t gen;
+    int32_t pad;
 };
 
-template <typename T, int R>
-__device__ __forceinline__ void cd_fill(CdEnt<T, R>& e, int64_t pos, int64_t tb, int64_t tend, const int32_t* As,
-                                        const T* __restrict__ X, int64_t ld, int n, const double* beta,
-                                        const double* __restrict__ nsq, const double* __restrict__ norms, int tid,
-                                        int BT) {
-    e.pos = pos;
-    if (pos < tend) {
-        const int32_t j = As[pos - tb];
-        e.j = j;
-        e.bj = beta[j];
-        e.ns = __ldg(nsq + j);
-        e.nr = __ldg(norms + j);
-        const T* x = X + (int64_t)j * ld;
-#pragma unroll
-        for (int k = 0; k < R; ++k) { const int r = tid + k * BT; e.x[k] = r < n ? to_d(__ldg(x + r)) : 0.0; }
+struct alignas(16) CdCtl {
+    unsigned long long bar[kRingMax];    // mbarriers (TMA completion), one per slot
+    int ready[kRingMax];                  // entry index + 1 published for the slot
+    int consumed[8];                      // per compute warp: entries fully read
+    double dpub;                          // Delta published by compute warp 0
+    int req_gen, req_pos;                 // restart request (compute -> producer)
+    int finished, pad0, pad1, pad2;       // compute warps consumed the current-generation end entry
+};
+
+// bounded spin: a protocol error traps (launch failure) instead of hanging the GPU
+__device__ __forceinline__ void spin_guard(unsigned long long t0) {
+    if (gtimer() - t0 > 20000000000ull) __trap();
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(unsigned long long* b, unsigned parity) {
+    unsigned ok;
+    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ double ld_vol(const double* p) { return *(const volatile double*)p; }
+
+// first position in [from, lim) with !(D < t) (uncertified under D)
+__device__ __forceinline__ int scan_under(const float* ts, int tb, int lim, int from, double D, int lane) {
+    for (int base = from; base < lim; base += 32) {
+        const int q = base + lane;
+        const bool unc = q < lim && !(D < (double)ts[q - tb]);
+        const unsigned b = __ballot_sync(0xffffffffu, unc);
+        if (b) return base + __ffs(b) - 1;
     }
+    return lim;
+}
+
+__host__ __device__ inline int cd_ring_slots(int64_t ld, int es) {
+    const int64_t bytes = ld * es;
+    return bytes <= 2048 ? 16 : (bytes <= 16384 ? 8 : 4);
+}
+__host__ __device__ inline size_t cd_slot_bytes(int64_t ld, int es) {
+    return sizeof(SlotHdr) + (size_t)ld * es;          // ld * es is a multiple of 16
+}
+__host__ __device__ inline size_t cd_smem_bytes_rt(int64_t ld, int es) {
+    return (size_t)kTTile * (sizeof(float) + sizeof(int32_t)) + 64 * sizeof(double) + sizeof(CdCtl) +
+           (size_t)cd_ring_slots(ld, es) * cd_slot_bytes(ld, es);
 }
 
 template <typename T, int R>
-__device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m, int W, unsigned char* smem,
+__device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int W, unsigned char* smem,
                                             int* tile_valid) {
     SolveCtl* ctl = P.ctl;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int BT = W * 32;
+    const int m = (int)m64;
     float* ts = reinterpret_cast<float*>(smem);
     int32_t* As = reinterpret_cast<int32_t*>(smem + kTTile * sizeof(float));
     double* part = reinterpret_cast<double*>(smem + kTTile * (sizeof(float) + sizeof(int32_t)));   // [2][32]
-    const T* __restrict__ X = (const T*)P.X;
+    CdCtl* cc = reinterpret_cast<CdCtl*>(part + 64);
+    unsigned char* ring = reinterpret_cast<unsigned char*>(cc + 1);
+    const int K = cd_ring_slots(P.ld, (int)sizeof(T));
+    const size_t sbytes = cd_slot_bytes(P.ld, (int)sizeof(T));
+    const unsigned xbytes = (unsigned)(P.ld * sizeof(T));
+    const bool use_t = P.certify != 0;
     const int n = P.n;
-    const int64_t ld = P.ld;
-    const int32_t* Ag = P.A;
-    float* tg = P.t;
-    double* beta = P.beta;
-    const double* __restrict__ nsq = P.nsq;
-    const double* __restrict__ norms = P.norms;
-    if (w < W && m > 0) {
+    if (m == 0) {
+        if (tid == 0) { ctl->epoch_unc = 0; ctl->epoch_nz = 0; }
+        __syncthreads();
+        return;
+    }
+    // ---- setup (all threads)
+    if (tid == 0) {
+        for (int s = 0; s < K; ++s) { mbar_init(&cc->bar[s], 1); cc->ready[s] = 0; }
+        for (int k = 0; k < 8; ++k) cc->consumed[k] = 0;
+        cc->dpub = use_t ? ctl->cd_delta : 0.0;
+        cc->req_gen = 0;
+        cc->req_pos = 0;
+        cc->finished = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const bool keep_tile = (m <= kTTile) && *tile_valid;
+    if (!keep_tile) {
+        const int lim = min(m, kTTile);
+        for (int q = tid; q < lim; q += blockDim.x) {
+            As[q] = P.A[q];
+            ts[q] = use_t ? P.t[q] : -1.0f;
+        }
+    }
+    __syncthreads();
+
+    if (w == W && W < (int)(blockDim.x >> 5)) {
+        // =================== producer warp ===================
+        const T* __restrict__ X = (const T*)P.X;
+        const ColInfo* __restrict__ cinfo = P.cinfo;
+        const double gs0 = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * P.lam;
+        const double margin_gs = __dmul_ru(4.0 * K, gs0);
+        int tb = 0, tend = min(m, kTTile);
+        int qnext = 0, gen = 0;
+        int k_issue = 0, k_pub = 0;
+        bool done = false;
+        const unsigned long long t0 = gtimer();
+        // runs until the compute warps consumed an end entry of the current
+        // generation: a restart can still arrive after the end entry was issued
+        while (!ld_vol(&cc->finished)) {
+            if (done && k_pub == k_issue) {
+                __nanosleep(64);
+                spin_guard(t0);
+            }
+            // restart request from the compute warps
+            const int rg = ld_vol(&cc->req_gen);
+            if (rg != gen) {
+                gen = rg;
+                const int rp = ld_vol(&cc->req_pos);
+                if (rp < tb || rp >= tend + (tend == m ? 1 : 0)) {
+                    // reload the tile containing rp (positions before tb are never revisited)
+                    tb = (rp / kTTile) * kTTile;
+                    tend = min(m, tb + kTTile);
+                    for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
+                    __syncwarp();
+                }
+                qnext = rp;
+                done = false;
+            }
+            // issue the next entry if its slot is free
+            if (!done && k_issue - k_pub < K) {
+                bool free_slot = true;
+                if (k_issue >= K) {
+                    const int need = k_issue - K + 1;
+                    for (int q = 0; q < W; ++q) free_slot &= ld_vol(&cc->consumed[q]) >= need;
+                    __threadfence_block();
+                }
+                if (!free_slot) __nanosleep(32);
+                if (free_slot) {
+                    const int s = k_issue % K;
+                    SlotHdr* h = reinterpret_cast<SlotHdr*>(ring + (size_t)s * sbytes);
+                    const double dp = use_t ? __dadd_ru(ld_vol(&cc->dpub), margin_gs) : 0.0;
+                    int p;
+                    while (true) {
+                        p = use_t ? scan_under(ts, tb, tend, qnext, dp, lane) : (qnext < tend ? qnext : tend);
+                        if (p < tend || tend >= m) break;
+                        // next tile
+                        tb = tend;
+                        tend = min(m, tb + kTTile);
+                        for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
+                        __syncwarp();
+                        qnext = tb;
+                    }
+                    if (lane == 0) {
+                        if (p < m) {
+                            const int32_t j = As[p - tb];
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            mbar_expect_tx(&cc->bar[s], xbytes + (unsigned)sizeof(ColInfo));
+                            tma_bulk_g2s(h + 1, X + (int64_t)j * P.ld, xbytes, &cc->bar[s]);
+                            tma_bulk_g2s(&h->ci, cinfo + j, (unsigned)sizeof(ColInfo), &cc->bar[s]);
+                            h->tcert = (double)ts[p - tb];
+                            h->dp = dp;
+                            h->j = j;
+                        } else {
+                            // end of the epoch: a plain arrive completes the phase
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&cc->bar[s])) : "memory");
+                        }
+                        h->pos = p;
+                        h->gen = gen;
+                    }
+                    __syncwarp();
+                    if (p >= m) done = true;
+                    qnext = p + 1;
+                    ++k_issue;
+                }
+            }
+            // publish completed entries in order
+            if (k_pub < k_issue) {
+                const int s = k_pub % K;
+                const unsigned parity = (unsigned)((k_pub / K) & 1);
+                int ok = 0;
+                if (lane == 0) ok = mbar_test(&cc->bar[s], parity);
+                ok = __shfl_sync(0xffffffffu, ok, 0);
+                if (ok) {
+                    if (lane == 0) {
+                        __threadfence_block();
+                        *(volatile int*)&cc->ready[s] = k_pub + 1;
+                    }
+                    ++k_pub;
+                }
+            }
+        }
+    } else if (w < W) {
+        // =================== compute warps ===================
         double rr[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) { const int r = tid + k * BT; rr[k] = r < n ? P.rho[r] : 0.0; }
-        const bool use_t = P.certify != 0;
         double D = use_t ? ctl->cd_delta : 0.0;
         const double rho0 = ctl->anchor_norm;
-        const double lam = P.lam;
-        int64_t tb = 0, tend = 0;
-        int pb = 0;
-        int64_t n_unc = 0, n_nz = 0;
-        auto load_tile = [&](int64_t from) {
-            tb = from;
-            tend = min(m, from + (int64_t)kTTile);
-            if (W > 1) named_bar(1, BT);
-#pragma unroll 4
-            for (int64_t q = tb + tid; q < tend; q += BT) {
-                As[q - tb] = Ag[q];
-                if (use_t) ts[q - tb] = tg[q];
+        double gstep = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * P.lam;
+        double* __restrict__ beta = P.beta;
+        ColInfo* cinfo_w = P.cinfo;
+        float* tg = P.t;
+        int pb = 0, gen = 0, last = -1;
+        int n_unc = 0, n_nz = 0, n_req = 0;
+        for (int k = 0;; ++k) {
+            const int s = k % K;
+            if (ld_vol(&cc->ready[s]) != k + 1) {
+                const unsigned long long t0 = gtimer();
+                while (ld_vol(&cc->ready[s]) != k + 1) spin_guard(t0);
             }
-            if (W > 1) named_bar(1, BT); else __syncwarp();
-        };
-        auto scan = [&](int64_t from, int64_t lim) -> int64_t {
-            if (from >= lim) return lim;
-            if (!use_t) return from;
-            return scan_tile(ts, tb, lim, from, D, lane);
-        };
-        auto fill = [&](CdEnt<T, R>& e, int64_t pos) { cd_fill<T, R>(e, pos, tb, tend, As, X, ld, n, beta, nsq, norms, tid, BT); };
-        CdEnt<T, R> ea, eb, ec;
-        auto prime = [&](int64_t from, CdEnt<T, R>& e0, CdEnt<T, R>& e1, CdEnt<T, R>& e2) {
-            while (true) {
-                const int64_t p0 = scan(from, tend);
-                if (p0 < tend || tend >= m) { fill(e0, p0); break; }
-                load_tile(tend);
-                from = tb;
-            }
-            fill(e1, scan(e0.pos + 1, tend));
-            fill(e2, scan(e1.pos + 1, tend));
-        };
-        // the tile of (index, threshold) stays resident across epochs while
-        // the active set and thresholds are unchanged and fit one tile
-        if (m <= kTTile && *tile_valid) {
-            tb = 0;
-            tend = m;
-        } else {
-            load_tile(0);
-        }
-        // one step on `cur`; afterwards the ring order is (nxt, nxt2, cur)
-        // with `cur` refilled as the third entry -- no register copies, so a
-        // prefetch issued two steps ahead is consumed two steps later.
-        auto step = [&](CdEnt<T, R>& cur, CdEnt<T, R>& nxt, CdEnt<T, R>& nxt2) -> bool {
-            if (cur.pos >= tend) {
-                if (tend >= m) return false;
-                prime(tend, cur, nxt, nxt2);
-                if (cur.pos >= tend) return false;
-            }
-            double acc = 0.0;
+            __threadfence_block();
+            const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
+            const int pos = h->pos;
+            const int hg = h->gen;
+            const double tc = h->tcert, dp = h->dp;
+            const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
+            const int32_t j = h->j;
+            const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
+            double xv[R];
 #pragma unroll
-            for (int k = 0; k < R; ++k) acc = fma(cur.x[k], rr[k], acc);
-            acc = warp_sum(acc);
+            for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
+            __syncwarp();
+            if (lane == 0) { __threadfence_block(); *(volatile int*)&cc->consumed[w] = k + 1; }   // slot fully read
+            if (hg != gen) continue;                                   // stale entry before a restart
+            if (pos >= m) {
+                if (tid == 0) { __threadfence_block(); *(volatile int*)&cc->finished = 1; }
+                break;
+            }
+            if (use_t) {
+                if (D > dp) {
+                    // drift outgrew the queue's bound: restart after the last processed position
+                    ++n_req;
+                    ++gen;
+                    if (tid == 0) { *(volatile int*)&cc->req_pos = last + 1; __threadfence_block(); *(volatile int*)&cc->req_gen = gen; }
+                    continue;
+                }
+                if (D < tc) continue;                                  // certified: zero update
+            }
+            // ---- critical chain
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < R; q += 2) {
+                a0 = fma(xv[q], rr[q], a0);
+                if (q + 1 < R) a1 = fma(xv[q + 1], rr[q + 1], a1);
+            }
+            double acc = warp_sum(a0 + a1);
             double g;
             if (W > 1) {
                 if (lane == 0) part[pb * 32 + w] = acc;
                 named_bar(1, BT);
                 g = 0.0;
-                for (int k = 0; k < W; ++k) g += part[pb * 32 + k];
+                for (int q = 0; q < W; ++q) g += part[pb * 32 + q];
                 pb ^= 1;
             } else {
                 g = acc;
             }
-            const double bj = cur.bj;
-            const double z = bj + g / cur.ns;
-            const double u = lam / cur.ns;
-            const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+            const double q0 = g * iv;
+            const double rq = fma(-q0, ns, g);
+            const double qq = fma(rq, iv, q0);            // RN(g / nsq)
+            const double z = bj + qq;
+            const double nb = z > uq ? z - uq : (z < -uq ? z + uq : 0.0);
             const double d = nb - bj;
             ++n_unc;
+            last = pos;
             if (d != 0.0) {
                 ++n_nz;
-                if (tid == 0) {
-                    beta[cur.j] = nb;
-                    if (use_t && bj == 0.0) tg[cur.pos] = -1.0f;   // now in the support
-                }
-                if (use_t && bj == 0.0) ts[cur.pos - tb] = -1.0f;  // (same value in every CD thread)
 #pragma unroll
-                for (int k = 0; k < R; ++k) rr[k] = __dsub_rn(rr[k], __dmul_rn(d, cur.x[k]));
+                for (int q = 0; q < R; ++q) rr[q] = __dsub_rn(rr[q], __dmul_rn(d, xv[q]));
                 if (use_t) {
-                    D = delta_step(D, __dmul_ru(fabs(d), cur.nr), rho0);
-                    // Delta grew: positions before the queued ones may now be uncertified
-                    const int64_t n1 = scan(cur.pos + 1, nxt.pos);
-                    if (n1 != nxt.pos) {
-                        fill(nxt, n1);
-                        fill(nxt2, scan(n1 + 1, tend));
-                        fill(cur, scan(nxt2.pos + 1, tend));
-                        return true;
+                    const double step = __dmul_ru(fabs(d), nr);
+                    D = delta_step(D, step, rho0);
+                    gstep = 0.875 * gstep + 0.125 * step;
+                }
+                if (tid == 0) {
+                    beta[j] = nb;
+                    cinfo_w[j].beta = nb;
+                    if (use_t && bj == 0.0) {
+                        tg[pos] = -1.0f;                       // now in the support
+                        if (m <= kTTile) ts[pos] = -1.0f;      // resident tile (single tile only)
                     }
-                    if (nxt.pos < tend) {
-                        const int64_t n2 = scan(nxt.pos + 1, nxt2.pos);
-                        if (n2 != nxt2.pos) fill(nxt2, n2);
-                    }
+                    *(volatile double*)&cc->dpub = D;
                 }
             }
-            fill(cur, scan(nxt2.pos + 1, tend));
-            return true;
-        };
-        prime(0, ea, eb, ec);
-        while (step(ea, eb, ec) && step(eb, ec, ea) && step(ec, ea, eb)) {
         }
         if (W > 1) named_bar(1, BT);
-        // write back rho, ||rho|| bound (next anchor), Delta, counters
-        double s = 0.0;
+        double s2 = 0.0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-            const int r = tid + k * BT;
-            if (r < n) { P.rho[r] = rr[k]; s = __dadd_ru(s, __dmul_ru(rr[k], rr[k])); }
+        for (int q = 0; q < R; ++q) {
+            const int r = tid + q * BT;
+            if (r < n) { P.rho[r] = rr[q]; s2 = __dadd_ru(s2, __dmul_ru(rr[q], rr[q])); }
         }
-        s = warp_sum_ru(s);
+        s2 = warp_sum_ru(s2);
         if (W > 1) {
-            if (lane == 0) part[pb * 32 + w] = s;
+            if (lane == 0) part[pb * 32 + w] = s2;
             named_bar(1, BT);
             double tot = 0.0;
-            for (int k = 0; k < W; ++k) tot = __dadd_ru(tot, part[pb * 32 + k]);
-            s = tot;
+            for (int q = 0; q < W; ++q) tot = __dadd_ru(tot, part[pb * 32 + q]);
+            s2 = tot;
         }
         if (tid == 0) {
-            P.sc->rho_norm_ub = __dsqrt_ru(s);
+            P.sc->rho_norm_ub = __dsqrt_ru(s2);
             ctl->cd_delta = D;
+            ctl->cd_gstep = gstep;
             ctl->epoch_unc = n_unc;
             ctl->epoch_nz = n_nz;
+            ctl->n_requeue += n_req;
             P.sc->visits += (unsigned long long)m;
             P.sc->uncertified += (unsigned long long)n_unc;
             P.sc->nonzero += (unsigned long long)n_nz;
-            *tile_valid = (m <= kTTile) ? 1 : 0;
         }
-    } else if (tid == 0 && m == 0) {
-        ctl->epoch_unc = 0;
-        ctl->epoch_nz = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        *tile_valid = (m <= kTTile) ? 1 : 0;
+        for (int s = 0; s < K; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&cc->bar[s])) : "memory");
     }
     __syncthreads();
 }
@@ -731,7 +907,7 @@ __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* sme
     DevScalars* sc = P.sc;
     SolveCtl* ctl = P.ctl;
     // dense: [CD tile | vs]; sparse: the CD uses [t tile | rho] and vs aliases it
-    double* vs = reinterpret_cast<double*>(smem + (P.sparse ? 0 : kCdBytes));
+    double* vs = reinterpret_cast<double*>(smem + (P.sparse ? 0 : P.cd_bytes));
     __shared__ int s_tile_valid;
     if (threadIdx.x == 0) s_tile_valid = 0;
     __syncthreads();
@@ -797,6 +973,17 @@ __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* sme
         for (int64_t j = (int64_t)g.c * blockDim.x + threadIdx.x; j < P.p; j += (int64_t)g.G * blockDim.x) {
             if (!P.mark[j]) P.beta[j] = 0.0;
             P.mark[j] = 0;
+            const double ns = __ldg(P.nsq + j);
+            if (!P.sparse) {
+                ColInfo ci;
+                ci.ns = ns;
+                ci.inv = __ldg(P.inv_nsq + j);
+                ci.nr = __ldg(P.norms + j);
+                ci.u = ns > 0.0 ? P.lam / ns : 0.0;   // u = lam / nsq (_kernels.py:51), per lambda
+                ci.beta = P.beta[j];
+                ci.pad = 0.0;
+                P.cinfo[j] = ci;
+            }
         }
         if (g.c == 0 && threadIdx.x == 0) {
             ctl->started = 1;
@@ -1035,12 +1222,21 @@ __global__ void __launch_bounds__(256, 1) k_cd_pass_prod(const SolveDev* __restr
     const SolveDev& P = probs[0];
     Group g{1, 0, nullptr};
     const int64_t m = P.sc->m;
+    if (!P.sparse)
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+            const int32_t j = P.A[i];
+            const double ns = __ldg(P.nsq + j);
+            ColInfo ci;
+            ci.ns = ns; ci.inv = __ldg(P.inv_nsq + j); ci.nr = __ldg(P.norms + j);
+            ci.u = ns > 0.0 ? P.lam / ns : 0.0; ci.beta = P.beta[j]; ci.pad = 0.0;
+            P.cinfo[j] = ci;
+        }
     double a = 0.0;
     for (int r = threadIdx.x; r < P.n; r += blockDim.x) { const double q = P.rho[r]; a = __dadd_ru(a, __dmul_ru(q, q)); }
     const double anchor = __dsqrt_ru(block_sum_ru(a, red));
     const double gam = gamma_n(P.n);
     if (P.certify) group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0,
-                                 reinterpret_cast<double*>(smem + (P.sparse ? 0 : kCdBytes)));
+                                 reinterpret_cast<double*>(smem + (P.sparse ? 0 : P.cd_bytes)));
     if (threadIdx.x == 0) { P.ctl->anchor_norm = anchor; P.ctl->cd_delta = 0.0; }
     __syncthreads();
     __shared__ int s_tile_valid;
