@@ -128,6 +128,8 @@ typedef struct {
     /* in-kernel phase times (device %globaltimer, ms) and counts */
     double screen_ms, ckpt_ms, refresh_ms, cd_ms;
     int64_t n_screen, n_refresh, launches;
+    /* CD pipeline: candidates fetched, skipped as certified, queue rebuilds */
+    int64_t cd_candidates, cd_skipped, cd_requeues;
 } gs_solve_result;
 
 /* y is uploaded once; lambda_max = |X^T y|_inf is computed once and cached
@@ -144,6 +146,19 @@ int gs_solver_seq_screen(gs_solver *S, double lam, int64_t *n_active);
 int gs_solver_solve(gs_solver *S, double lam, const gs_solve_config *cfg, const int64_t *active0,
                     int64_t n0, int active0_mode, gs_solve_result *res);
 void gs_solver_free(gs_solver *S);
+
+/* ---- batched independent problems (BASELINE configs[4]) ---- */
+/* B problems on row-resampled copies of one dense design: problem b uses rows
+ * rows[b*n .. b*n+n) of X0 (with repetition) and the same entries of y0.  Each
+ * problem runs its whole warm-started path in one CTA (device-side lambda loop). */
+typedef struct gs_batch gs_batch;
+int gs_batch_create(const gs_matrix *X0, const double *y0, const int32_t *rows, int64_t B, int64_t n,
+                    gs_batch **out);
+int gs_batch_lambda_max(gs_batch *Bt, double *lambda_max);      /* [B] */
+/* grids: [B*T] (each non-increasing).  Outputs [B*T] (betas [B*T*p], may be NULL). */
+int gs_batch_run_paths(gs_batch *Bt, const double *grids, int64_t T, const gs_solve_config *cfg, double *betas,
+                       int64_t *passes, double *gaps, int32_t *converged, int64_t *n_active, double *device_ms);
+void gs_batch_free(gs_batch *Bt);
 
 /* ---- measurement support ---------------------------------------------------- */
 /* CUDA events on the solver's stream: op 0 records the start, op 1 records the

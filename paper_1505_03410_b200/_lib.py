@@ -56,7 +56,8 @@ class SolveResult(ctypes.Structure):
                 ("cd_visits", ctypes.c_uint64), ("cd_uncertified", ctypes.c_uint64),
                 ("cd_nonzero", ctypes.c_uint64), ("checkpoints", c_i64), ("device_ms", c_dbl),
                 ("screen_ms", c_dbl), ("ckpt_ms", c_dbl), ("refresh_ms", c_dbl), ("cd_ms", c_dbl),
-                ("n_screen", c_i64), ("n_refresh", c_i64), ("launches", c_i64)]
+                ("n_screen", c_i64), ("n_refresh", c_i64), ("launches", c_i64),
+                ("cd_candidates", c_i64), ("cd_skipped", c_i64), ("cd_requeues", c_i64)]
 
 
 # every symbol declared in include/gapsafe_b200.h with its ctypes signature
@@ -89,6 +90,11 @@ SIGNATURES = {
     "gs_screen_timed": (c_i32, [c_vp, P_f64, c_dbl, ctypes.c_int, P_f64, P_i64]),
     "gs_host_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
     "gs_host_free": (None, [c_vp]),
+    "gs_batch_create": (c_i32, [c_vp, P_f64, P_i32, c_i64, c_i64, ctypes.POINTER(c_vp)]),
+    "gs_batch_lambda_max": (c_i32, [c_vp, P_f64]),
+    "gs_batch_run_paths": (c_i32, [c_vp, P_f64, c_i64, ctypes.POINTER(SolveConfig), P_f64, P_i64, P_f64,
+                                   P_i32, P_i64, P_f64]),
+    "gs_batch_free": (None, [c_vp]),
 }
 
 _lib = None

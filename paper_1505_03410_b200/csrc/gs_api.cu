@@ -922,6 +922,7 @@ extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* 
     R->screen_ms = c->t_screen * 1e-6; R->ckpt_ms = c->t_ckpt * 1e-6;
     R->refresh_ms = c->t_refresh * 1e-6; R->cd_ms = c->t_cd * 1e-6;
     R->n_screen = c->n_screen; R->n_refresh = c->n_refresh; R->launches = launches;
+    R->cd_candidates = c->n_cand; R->cd_skipped = c->n_skip; R->cd_requeues = c->n_requeue;
     TRY(solve_outputs(S, R, c->ntrace, S->m));
     S->has_prev = true; S->prev_margin = h->margin; S->prev_interp = h->interp;
     CK(cudaEventRecord(S->ev1, st));
@@ -1112,3 +1113,251 @@ extern "C" int gs_host_alloc(int64_t bytes, void** out) {
 }
 
 extern "C" void gs_host_free(void* ptr) { cudaFreeHost(ptr); }
+
+// ---------------------------------------------------------------------------
+// batched independent problems (cfg4): one CTA per problem, whole path on device
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ X0, int64_t ld0, const int32_t* __restrict__ rows, int n,
+                              int64_t ld, int64_t p, int64_t B, T* __restrict__ Xb) {
+    // block (j-chunk, b); threads over rows
+    const int64_t b = blockIdx.y;
+    const int32_t* rw = rows + b * n;
+    T* dst = Xb + b * ld * p;
+    for (int64_t j = blockIdx.x; j < p; j += gridDim.x) {
+        const T* col = X0 + j * ld0;
+        for (int r = threadIdx.x; r < ld; r += blockDim.x) dst[j * ld + r] = r < n ? col[rw[r]] : (T)0;
+    }
+}
+
+__global__ void k_gather_y(const double* __restrict__ y0, const int32_t* __restrict__ rows, int n, int64_t B,
+                           double* __restrict__ yb, int64_t ldy) {
+    const int64_t b = blockIdx.x;
+    for (int r = threadIdx.x; r < ldy; r += blockDim.x) yb[b * ldy + r] = r < n ? y0[rows[b * n + r]] : 0.0;
+}
+
+struct gs_batch {
+    int64_t B = 0, n = 0, p = 0, ld = 0, ldy = 0;
+    int dtype = GS_DTYPE_F64;
+    gs_matrix shape;                  // shape descriptor (no storage) for launch configuration
+    void* X = nullptr;                // B designs, column-major, ld rows each
+    double *y = nullptr, *norms_sq = nullptr, *norms = nullptr, *inv = nullptr;
+    double *beta = nullptr, *rho = nullptr, *theta = nullptr, *c = nullptr;
+    ColInfo* cinfo = nullptr;
+    float *t = nullptr, *t2 = nullptr;
+    int32_t *A = nullptr, *A2 = nullptr, *S = nullptr, *Dl = nullptr;
+    uint8_t* mark = nullptr;
+    double* partial = nullptr;
+    int nch_max = 1;
+    DevScalars* sc = nullptr;
+    SolveCtl* ctl = nullptr;
+    TraceRow* trace = nullptr;
+    int64_t trace_cap = 0;
+    double* cta_val = nullptr;
+    int64_t* cta_idx = nullptr;
+    int64_t* cta_cnt = nullptr;
+    SolveDev* dprobs = nullptr;
+    BatchOut* douts = nullptr;
+    std::vector<double> lmax;
+    std::vector<double> ynsq;
+    cudaStream_t st = nullptr;
+};
+
+static void batch_release(gs_batch* Bt) {
+    if (!Bt) return;
+    void* ptrs[] = {Bt->X, Bt->y, Bt->norms_sq, Bt->norms, Bt->inv, Bt->beta, Bt->rho, Bt->theta, Bt->c,
+                    Bt->cinfo, Bt->t, Bt->t2, Bt->A, Bt->A2, Bt->S, Bt->Dl, Bt->mark, Bt->partial, Bt->sc,
+                    Bt->ctl, Bt->trace, Bt->cta_val, Bt->cta_idx, Bt->cta_cnt, Bt->dprobs, Bt->douts};
+    for (void* q : ptrs) cudaFree(q);
+    if (Bt->st) cudaStreamDestroy(Bt->st);
+    delete Bt;
+}
+
+extern "C" int gs_batch_create(const gs_matrix* X0, const double* y0, const int32_t* rows, int64_t B, int64_t n,
+                               gs_batch** out) {
+    TRY(ensure_device());
+    if (X0->sparse) return fail(GS_ERR_VALUE, "batched problems need a dense design");
+    if (B < 1 || n < 1) return fail(GS_ERR_VALUE, "batch needs B >= 1 problems of n >= 1 rows");
+    for (int64_t i = 0; i < B * n; ++i)
+        if (rows[i] < 0 || rows[i] >= X0->n) return fail(GS_ERR_INDEX, "row index out of range");
+    gs_batch* Bt = new gs_batch();
+    int rc = [&]() -> int {
+        Bt->B = B; Bt->n = n; Bt->p = X0->p; Bt->dtype = X0->dtype;
+        const int64_t align = X0->dtype == GS_DTYPE_F64 ? 2 : 4;
+        Bt->ld = (n + align - 1) / align * align;
+        Bt->ldy = n + 2;
+        Bt->shape.n = n; Bt->shape.p = X0->p; Bt->shape.ld = Bt->ld; Bt->shape.dtype = X0->dtype;
+        if (cd_shape(n).R == 0) return fail(GS_ERR_VALUE, "batched solver supports n <= 1792");
+        const int64_t p = Bt->p, ld = Bt->ld;
+        const size_t es = X0->dtype == GS_DTYPE_F64 ? 8 : 4;
+        CK(cudaStreamCreateWithFlags(&Bt->st, cudaStreamNonBlocking));
+        cudaStream_t st = Bt->st;
+        CK(cudaMalloc(&Bt->X, (size_t)B * ld * p * es));
+        TRY(dalloc(&Bt->y, B * Bt->ldy)); TRY(dalloc(&Bt->norms_sq, B * p)); TRY(dalloc(&Bt->norms, B * p));
+        TRY(dalloc(&Bt->inv, B * p)); TRY(dalloc(&Bt->beta, B * p)); TRY(dalloc(&Bt->rho, B * Bt->ldy));
+        TRY(dalloc(&Bt->theta, B * Bt->ldy)); TRY(dalloc(&Bt->c, B * p)); TRY(dalloc(&Bt->cinfo, B * p));
+        TRY(dalloc(&Bt->t, B * p)); TRY(dalloc(&Bt->t2, B * p)); TRY(dalloc(&Bt->A, B * p));
+        TRY(dalloc(&Bt->A2, B * p)); TRY(dalloc(&Bt->S, B * p)); TRY(dalloc(&Bt->Dl, B * p));
+        TRY(dalloc(&Bt->mark, B * p));
+        Bt->nch_max = (int)std::min<int64_t>(32, std::max<int64_t>(1, (p + 15) / 16));
+        TRY(dalloc(&Bt->partial, B * Bt->nch_max * n));
+        TRY(dalloc(&Bt->sc, B)); TRY(dalloc(&Bt->ctl, B));
+        TRY(dalloc(&Bt->cta_val, B)); TRY(dalloc(&Bt->cta_idx, B)); TRY(dalloc(&Bt->cta_cnt, 2 * B));
+        TRY(dalloc(&Bt->dprobs, B)); TRY(dalloc(&Bt->douts, B));
+        CK(cudaMemsetAsync(Bt->mark, 0, B * p, st));
+        CK(cudaMemsetAsync(Bt->beta, 0, B * p * 8, st));
+        CK(cudaMemsetAsync(Bt->rho, 0, B * Bt->ldy * 8, st));
+        CK(cudaMemsetAsync(Bt->theta, 0, B * Bt->ldy * 8, st));
+        CK(cudaMemsetAsync(Bt->sc, 0, B * sizeof(DevScalars), st));
+        int32_t* drows;
+        TRY(dalloc(&drows, B * n));
+        CK(cudaMemcpyAsync(drows, rows, B * n * 4, cudaMemcpyHostToDevice, st));
+        double* dy0;
+        TRY(dalloc(&dy0, X0->n));
+        CK(cudaMemcpyAsync(dy0, y0, X0->n * 8, cudaMemcpyHostToDevice, st));
+        dim3 gg((unsigned)std::min<int64_t>(p, 4096), (unsigned)B);
+        if (X0->dtype == GS_DTYPE_F64)
+            k_gather_rows<double><<<gg, 256, 0, st>>>((const double*)X0->X, X0->ld, drows, (int)n, ld, p, B, (double*)Bt->X);
+        else
+            k_gather_rows<float><<<gg, 256, 0, st>>>((const float*)X0->X, X0->ld, drows, (int)n, ld, p, B, (float*)Bt->X);
+        k_gather_y<<<(unsigned)B, 256, 0, st>>>(dy0, drows, (int)n, B, Bt->y, Bt->ldy);
+        CKL();
+        // column norms of all B * p columns at once
+        if (X0->dtype == GS_DTYPE_F64)
+            k_col_norms_sq_dense<double><<<grid_for(B * p * 32, 256), 256, 0, st>>>((const double*)Bt->X, ld, (int)n, B * p, Bt->norms_sq);
+        else
+            k_col_norms_sq_dense<float><<<grid_for(B * p * 32, 256), 256, 0, st>>>((const float*)Bt->X, ld, (int)n, B * p, Bt->norms_sq);
+        k_sqrt_vec<<<grid_for(B * p, 256), 256, 0, st>>>(Bt->norms_sq, 0.0, B * p, Bt->norms_sq, Bt->norms, Bt->inv);
+        CKL();
+        // lambda_max and ||y||^2 per problem
+        Scratch sc;
+        TRY(sc.alloc(p));
+        double *dval, *dvs;
+        int64_t* didx;
+        TRY(dalloc(&dval, B)); TRY(dalloc(&didx, B)); TRY(dalloc(&dvs, 2 * B));
+        for (int64_t b = 0; b < B; ++b) {
+            gs_matrix Mb = Bt->shape;
+            Mb.X = (char*)Bt->X + (size_t)b * ld * p * es;
+            GemvArgs a{};
+            a.v = Bt->y + b * Bt->ldy; a.m = p; a.mode = GEMV_MAX; a.blk_val = sc.blk_val; a.blk_idx = sc.blk_idx;
+            int64_t nb = 0;
+            TRY(launch_gemv(&Mb, st, a, &nb));
+            k_max_finalize<<<1, 1024, 0, st>>>(sc.blk_val, sc.blk_idx, nb, dval + b, didx + b);
+            k_vec_stats<<<1, 1024, 0, st>>>(Bt->y + b * Bt->ldy, Bt->y + b * Bt->ldy, n, dvs + 2 * b);
+        }
+        CKL();
+        Bt->lmax.resize(B);
+        std::vector<double> vs(2 * B);
+        CK(cudaMemcpyAsync(Bt->lmax.data(), dval, B * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(vs.data(), dvs, 2 * B * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        Bt->ynsq.resize(B);
+        for (int64_t b = 0; b < B; ++b) Bt->ynsq[b] = vs[2 * b];
+        sc.release();
+        cudaFree(dval); cudaFree(didx); cudaFree(dvs); cudaFree(drows); cudaFree(dy0);
+        return GS_OK;
+    }();
+    if (rc != GS_OK) { batch_release(Bt); return rc; }
+    *out = Bt;
+    return GS_OK;
+}
+
+extern "C" int gs_batch_lambda_max(gs_batch* Bt, double* lmax) {
+    for (int64_t b = 0; b < Bt->B; ++b) lmax[b] = Bt->lmax[b];
+    return GS_OK;
+}
+
+extern "C" void gs_batch_free(gs_batch* Bt) { batch_release(Bt); }
+
+extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, const gs_solve_config* cfg,
+                                  double* betas, int64_t* passes, double* gaps, int32_t* converged,
+                                  int64_t* n_active, double* device_ms) {
+    if (cfg->epsilon <= 0) return fail(GS_ERR_VALUE, "epsilon must be positive");
+    if (cfg->screen_every < 1 || cfg->max_passes < 1) return fail(GS_ERR_VALUE, "bad solver configuration");
+    if (cfg->on_checkpoint) return fail(GS_ERR_VALUE, "checkpoint hooks are not available in batched mode");
+    const int64_t B = Bt->B, p = Bt->p, n = Bt->n, ld = Bt->ld;
+    cudaStream_t st = Bt->st;
+    const size_t es = Bt->dtype == GS_DTYPE_F64 ? 8 : 4;
+    const int64_t cap = cfg->max_passes / cfg->screen_every + 4;
+    if (cap * B > Bt->trace_cap) {
+        cudaFree(Bt->trace);
+        TRY(dalloc(&Bt->trace, cap * B));
+        Bt->trace_cap = cap * B;
+    }
+    double *dgrid, *dbetas = nullptr, *dgaps;
+    int64_t *dpasses, *dnact;
+    int32_t* dconv;
+    TmpBuf tb;
+    TRY(tb.get(&dgrid, B * T)); TRY(tb.get(&dgaps, B * T)); TRY(tb.get(&dpasses, B * T));
+    TRY(tb.get(&dnact, B * T)); TRY(tb.get(&dconv, B * T));
+    if (betas) TRY(tb.get(&dbetas, B * T * p));
+    CK(cudaMemcpyAsync(dgrid, grids, B * T * 8, cudaMemcpyHostToDevice, st));
+    std::vector<SolveDev> probs(B);
+    std::vector<BatchOut> outs(B);
+    std::vector<DevScalars> hsc(B);
+    const CdShape cs = cd_shape(n);
+    for (int64_t b = 0; b < B; ++b) {
+        SolveDev& d = probs[b];
+        memset(&d, 0, sizeof d);
+        d.X = (char*)Bt->X + (size_t)b * ld * p * es; d.ld = ld; d.n = (int)n; d.dtype = Bt->dtype; d.p = p;
+        d.norms = Bt->norms + b * p; d.nsq = Bt->norms_sq + b * p; d.inv_nsq = Bt->inv + b * p;
+        d.y = Bt->y + b * Bt->ldy; d.beta = Bt->beta + b * p; d.rho = Bt->rho + b * Bt->ldy;
+        d.theta = Bt->theta + b * Bt->ldy; d.cinfo = Bt->cinfo + b * p; d.c = Bt->c + b * p;
+        d.t = Bt->t + b * p; d.t2 = Bt->t2 + b * p; d.A = Bt->A + b * p; d.A2 = Bt->A2 + b * p;
+        d.S = Bt->S + b * p; d.Dl = Bt->Dl + b * p; d.mark = Bt->mark + b * p;
+        d.partial = Bt->partial + b * Bt->nch_max * n; d.nch_max = Bt->nch_max;
+        d.sc = Bt->sc + b; d.ctl = Bt->ctl + b; d.trace = Bt->trace + b * cap; d.trace_cap = cap;
+        d.cta_val = Bt->cta_val + b; d.cta_idx = Bt->cta_idx + b; d.cta_cnt = Bt->cta_cnt + 2 * b;
+        d.eps = cfg->epsilon; d.max_passes = cfg->max_passes; d.f = cfg->screen_every; d.rule = cfg->rule;
+        d.certify = cfg->certify; d.cd_warps = cs.W; d.cd_bytes = (int)cd_bytes_for(&Bt->shape);
+        d.vs_cap = vs_cap_for(&Bt->shape);
+        const char* env = getenv("GS_REFRESH_EXCESS");
+        d.refresh_excess = env ? atoi(env) : 32;
+        BatchOut& o = outs[b];
+        o.grid = dgrid + b * T; o.lmax = Bt->lmax[b]; o.betas = dbetas ? dbetas + b * T * p : nullptr;
+        o.passes = dpasses + b * T; o.gaps = dgaps + b * T; o.converged = dconv + b * T; o.n_active = dnact + b * T;
+        o.T = (int)T;
+        memset(&hsc[b], 0, sizeof(DevScalars));
+        hsc[b].eps = cfg->epsilon; hsc[b].y_norm_sq = Bt->ynsq[b];
+    }
+    CK(cudaMemcpyAsync(Bt->dprobs, probs.data(), B * sizeof(SolveDev), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(Bt->douts, outs.data(), B * sizeof(BatchOut), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(Bt->sc, hsc.data(), B * sizeof(DevScalars), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(Bt->beta, 0, B * p * 8, st));
+    const size_t smem = solve_smem(&Bt->shape);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    COUNT_LAUNCH(1);
+    const bool f64 = Bt->dtype == GS_DTYPE_F64;
+#define GS_BATCH_LAUNCH(TT, RR)                                                                          \
+    do {                                                                                                  \
+        CK(cudaFuncSetAttribute(k_batch_path<TT, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_batch_path<TT, RR><<<(unsigned)B, kSolveThreads, smem, st>>>(Bt->dprobs, Bt->douts);           \
+    } while (0)
+    if (f64) {
+        switch (cs.R) { case 1: GS_BATCH_LAUNCH(double, 1); break; case 2: GS_BATCH_LAUNCH(double, 2); break;
+                        case 4: GS_BATCH_LAUNCH(double, 4); break; default: GS_BATCH_LAUNCH(double, 8); }
+    } else {
+        switch (cs.R) { case 1: GS_BATCH_LAUNCH(float, 1); break; case 2: GS_BATCH_LAUNCH(float, 2); break;
+                        case 4: GS_BATCH_LAUNCH(float, 4); break; default: GS_BATCH_LAUNCH(float, 8); }
+    }
+#undef GS_BATCH_LAUNCH
+    CKL();
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (device_ms) *device_ms = ms;
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    if (passes) CK(cudaMemcpyAsync(passes, dpasses, B * T * 8, cudaMemcpyDeviceToHost, st));
+    if (gaps) CK(cudaMemcpyAsync(gaps, dgaps, B * T * 8, cudaMemcpyDeviceToHost, st));
+    if (converged) CK(cudaMemcpyAsync(converged, dconv, B * T * 4, cudaMemcpyDeviceToHost, st));
+    if (n_active) CK(cudaMemcpyAsync(n_active, dnact, B * T * 8, cudaMemcpyDeviceToHost, st));
+    if (betas) CK(cudaMemcpyAsync(betas, dbetas, B * T * p * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (converged)
+        for (int64_t i = 0; i < B * T; ++i)
+            if (converged[i] < 0) return fail(GS_ERR_NUMERICAL, "a batched problem hit an infeasible / negative-gap status");
+    return GS_OK;
+}

@@ -38,7 +38,7 @@ struct SolveCtl {
     int64_t k, passes, ntrace, nckpt;
     int32_t started, resume, pending, done, converged, status, need_refresh, final_done;
     double cd_delta, anchor_norm, cd_gstep;
-    int64_t n_requeue;
+    int64_t n_requeue, n_cand, n_skip;
     int64_t epoch_unc, epoch_nz;
     int64_t n_refresh;
     // device-side phase timers (%globaltimer, ns), CTA 0 thread 0
@@ -464,24 +464,25 @@ __device__ __forceinline__ double delta_step(double D, double step, double rho0)
 
 // Serial CD chain, warp-specialized.
 //
-//   producer warp (warp W):  scans the staged thresholds for the next
-//     candidates -- positions uncertified under a pessimistic drift bound
-//     Dp = Delta_published + margin -- and for each one issues two TMA bulk
-//     copies (cp.async.bulk, mbarrier complete_tx) into a ring slot: the
-//     column x_j (contiguous, ld*sizeof(T) bytes) and its packed ColInfo
-//     (nsq, 1/nsq, ||x||, u = lam/nsq, beta).  It then writes the slot header
-//     (position, threshold, Dp, generation), waits for the bytes in order and
-//     publishes ready[slot].
-//   compute warps (0..W-1):  poll ready[slot]; skip candidates certified under
-//     the current Delta; otherwise run the chain  dot -> butterfly [-> cross-
-//     warp sum] -> RN(g/nsq) (RN(1/nsq) + Markstein) -> soft threshold -> axpy,
-//     then publish Delta.  If Delta outgrew an entry's Dp, the positions between
-//     candidates may no longer be certified: they request a restart at the
-//     last processed position + 1 with a new generation and drain stale entries.
+//   producer warp (warp W): one ballot over 32 staged thresholds yields every
+//     candidate in the window -- positions uncertified under a pessimistic
+//     drift bound Dp = Delta_published + margin.  Each lane then issues its own
+//     candidate into its own ring slot: two TMA bulk copies (cp.async.bulk,
+//     mbarrier complete_tx) for the column x_j (ld*sizeof(T) bytes) and its
+//     packed ColInfo (nsq, 1/nsq, ||x||, u = lam/nsq, beta), then the slot
+//     header (position, threshold, Dp, generation).  Headers are published at
+//     once (hdr_ready); data readiness is published in order as the TMA
+//     transactions complete (data_ready).
+//   compute warps (0..W-1): read the next header; skip candidates certified
+//     under the current Delta without waiting for their data; otherwise wait
+//     for data_ready and run the chain  dot -> butterfly [-> cross-warp sum] ->
+//     RN(g/nsq) (RN(1/nsq) + Markstein) -> soft threshold -> axpy, then publish
+//     Delta.  If Delta outgrew an entry's Dp, positions between candidates may
+//     no longer be certified: restart after the last processed position with a
+//     new generation; stale entries are drained.
 // Candidates are consumed strictly in ascending position order, so the
 // arithmetic is exactly the sequential CD over the uncertified positions.
-constexpr int kRingMax = 16;
-
+constexpr int kRingMax = 64;
 
 struct alignas(16) SlotHdr {
     ColInfo ci;                      // TMA destination (48 B)
@@ -494,8 +495,9 @@ struct alignas(16) SlotHdr {
 };
 
 struct alignas(16) CdCtl {
-    unsigned long long bar[kRingMax];    // mbarriers (TMA completion), one per slot
-    int ready[kRingMax];                  // entry index + 1 published for the slot
+    unsigned long long bar[kRingMax];     // mbarriers (TMA completion), one per slot
+    int hdr_ready[kRingMax];              // entry index + 1 whose header is in the slot
+    int data_ready[kRingMax];             // entry index + 1 whose bytes have landed
     int consumed[8];                      // per compute warp: entries fully read
     double dpub;                          // Delta published by compute warp 0
     int req_gen, req_pos;                 // restart request (compute -> producer)
@@ -512,21 +514,23 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)_
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+__device__ __forceinline__ void mbar_expect_tx_s(unsigned b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ bool mbar_test(unsigned long long* b, unsigned parity) {
+__device__ __forceinline__ void mbar_arrive_s(unsigned b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ bool mbar_test_s(unsigned b, unsigned parity) {
     unsigned ok;
     asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+                 : "=r"(ok) : "r"(b), "r"(parity) : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+__device__ __forceinline__ void tma_bulk_g2s_s(unsigned dst, const void* src, unsigned bytes, unsigned b) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(b) : "memory");
 }
 __device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
-__device__ __forceinline__ double ld_vol(const double* p) { return *(const volatile double*)p; }
 
 // first position in [from, lim) with !(D < t) (uncertified under D)
 __device__ __forceinline__ int scan_under(const float* ts, int tb, int lim, int from, double D, int lane) {
@@ -540,8 +544,11 @@ __device__ __forceinline__ int scan_under(const float* ts, int tb, int lim, int 
 }
 
 __host__ __device__ inline int cd_ring_slots(int64_t ld, int es) {
-    const int64_t bytes = ld * es;
-    return bytes <= 2048 ? 16 : (bytes <= 16384 ? 8 : 4);
+    // power of two, at most 64 slots and ~128 KB of ring
+    const int64_t bytes = ld * es + 80;
+    int k = 64;
+    while (k > 4 && (int64_t)k * bytes > 128 * 1024) k >>= 1;
+    return k;
 }
 __host__ __device__ inline size_t cd_slot_bytes(int64_t ld, int es) {
     return sizeof(SlotHdr) + (size_t)ld * es;          // ld * es is a multiple of 16
@@ -563,8 +570,9 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
     double* part = reinterpret_cast<double*>(smem + kTTile * (sizeof(float) + sizeof(int32_t)));   // [2][32]
     CdCtl* cc = reinterpret_cast<CdCtl*>(part + 64);
     unsigned char* ring = reinterpret_cast<unsigned char*>(cc + 1);
-    const int K = cd_ring_slots(P.ld, (int)sizeof(T));
-    const size_t sbytes = cd_slot_bytes(P.ld, (int)sizeof(T));
+    const int K = cd_ring_slots(P.ld, (int)sizeof(T));          // power of two
+    const int kmask = K - 1, kshift = __ffs(K) - 1;
+    const unsigned sbytes = (unsigned)cd_slot_bytes(P.ld, (int)sizeof(T));
     const unsigned xbytes = (unsigned)(P.ld * sizeof(T));
     const bool use_t = P.certify != 0;
     const int n = P.n;
@@ -575,7 +583,7 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
     }
     // ---- setup (all threads)
     if (tid == 0) {
-        for (int s = 0; s < K; ++s) { mbar_init(&cc->bar[s], 1); cc->ready[s] = 0; }
+        for (int s = 0; s < K; ++s) { mbar_init(&cc->bar[s], 1); cc->hdr_ready[s] = 0; cc->data_ready[s] = 0; }
         for (int k = 0; k < 8; ++k) cc->consumed[k] = 0;
         cc->dpub = use_t ? ctl->cd_delta : 0.0;
         cc->req_gen = 0;
@@ -592,102 +600,133 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
         }
     }
     __syncthreads();
+    const unsigned ring_s = smem_u32(ring);
+    const unsigned bar_s = smem_u32(&cc->bar[0]);
 
     if (w == W && W < (int)(blockDim.x >> 5)) {
         // =================== producer warp ===================
         const T* __restrict__ X = (const T*)P.X;
         const ColInfo* __restrict__ cinfo = P.cinfo;
         const double gs0 = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * P.lam;
-        const double margin_gs = __dmul_ru(4.0 * K, gs0);
+        const double margin_gs = __dmul_ru(2.0 * K, gs0);
         int tb = 0, tend = min(m, kTTile);
         int qnext = 0, gen = 0;
-        int k_issue = 0, k_pub = 0;
+        int k_issue = 0, k_data = 0;       // entries issued / data published
         bool done = false;
-        const unsigned long long t0 = gtimer();
-        // runs until the compute warps consumed an end entry of the current
-        // generation: a restart can still arrive after the end entry was issued
+        unsigned long long t0 = gtimer();       // reset on progress (watchdog)
+        auto load_tile_p = [&](int from) {
+            tb = (from / kTTile) * kTTile;
+            tend = min(m, tb + kTTile);
+            for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
+            __syncwarp();
+        };
         while (!ld_vol(&cc->finished)) {
-            if (done && k_pub == k_issue) {
-                __nanosleep(64);
-                spin_guard(t0);
-            }
             // restart request from the compute warps
             const int rg = ld_vol(&cc->req_gen);
             if (rg != gen) {
+                __threadfence_block();
                 gen = rg;
                 const int rp = ld_vol(&cc->req_pos);
-                if (rp < tb || rp >= tend + (tend == m ? 1 : 0)) {
-                    // reload the tile containing rp (positions before tb are never revisited)
-                    tb = (rp / kTTile) * kTTile;
-                    tend = min(m, tb + kTTile);
-                    for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
-                    __syncwarp();
-                }
+                if (rp < tb || rp > tend || (rp == tend && tend < m)) load_tile_p(rp);
                 qnext = rp;
                 done = false;
             }
-            // issue the next entry if its slot is free
-            if (!done && k_issue - k_pub < K) {
-                bool free_slot = true;
-                if (k_issue >= K) {
-                    const int need = k_issue - K + 1;
-                    for (int q = 0; q < W; ++q) free_slot &= ld_vol(&cc->consumed[q]) >= need;
-                    __threadfence_block();
-                }
-                if (!free_slot) __nanosleep(32);
-                if (free_slot) {
-                    const int s = k_issue % K;
-                    SlotHdr* h = reinterpret_cast<SlotHdr*>(ring + (size_t)s * sbytes);
-                    const double dp = use_t ? __dadd_ru(ld_vol(&cc->dpub), margin_gs) : 0.0;
-                    int p;
-                    while (true) {
-                        p = use_t ? scan_under(ts, tb, tend, qnext, dp, lane) : (qnext < tend ? qnext : tend);
-                        if (p < tend || tend >= m) break;
-                        // next tile
-                        tb = tend;
-                        tend = min(m, tb + kTTile);
-                        for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
-                        __syncwarp();
-                        qnext = tb;
-                    }
-                    if (lane == 0) {
-                        if (p < m) {
-                            const int32_t j = As[p - tb];
-                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                            mbar_expect_tx(&cc->bar[s], xbytes + (unsigned)sizeof(ColInfo));
-                            tma_bulk_g2s(h + 1, X + (int64_t)j * P.ld, xbytes, &cc->bar[s]);
-                            tma_bulk_g2s(&h->ci, cinfo + j, (unsigned)sizeof(ColInfo), &cc->bar[s]);
-                            h->tcert = (double)ts[p - tb];
-                            h->dp = dp;
-                            h->j = j;
-                        } else {
-                            // end of the epoch: a plain arrive completes the phase
-                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&cc->bar[s])) : "memory");
-                        }
-                        h->pos = p;
-                        h->gen = gen;
-                    }
-                    __syncwarp();
-                    if (p >= m) done = true;
-                    qnext = p + 1;
-                    ++k_issue;
-                }
-            }
-            // publish completed entries in order
-            if (k_pub < k_issue) {
-                const int s = k_pub % K;
-                const unsigned parity = (unsigned)((k_pub / K) & 1);
+            // data readiness, in order
+            while (k_data < k_issue) {
+                const int s = k_data & kmask;
                 int ok = 0;
-                if (lane == 0) ok = mbar_test(&cc->bar[s], parity);
+                if (lane == 0) ok = mbar_test_s(bar_s + 8u * s, (unsigned)((k_data >> kshift) & 1));
                 ok = __shfl_sync(0xffffffffu, ok, 0);
-                if (ok) {
-                    if (lane == 0) {
-                        __threadfence_block();
-                        *(volatile int*)&cc->ready[s] = k_pub + 1;
-                    }
-                    ++k_pub;
-                }
+                if (!ok) break;
+                if (lane == 0) { __threadfence_block(); *(volatile int*)&cc->data_ready[s] = k_data + 1; }
+                ++k_data;
+                t0 = gtimer();
             }
+            // free slots: entries consumed by every compute warp and whose bytes landed
+            int cmin = 0x7fffffff;
+            for (int q = 0; q < W; ++q) cmin = min(cmin, ld_vol(&cc->consumed[q]));
+            const int free_slots = min(K - (k_issue - cmin), K - (k_issue - k_data));
+            if (done || free_slots <= 0) {
+                __nanosleep(32);
+                spin_guard(t0);
+                continue;
+            }
+            __threadfence_block();
+            // one ballot: every candidate of the next window
+            const double dp = use_t ? __dadd_ru(*(const volatile double*)&cc->dpub, margin_gs) : 0.0;
+            int base = qnext;
+            unsigned mask = 0;
+            while (true) {
+                if (base >= tend) {
+                    if (tend >= m) break;
+                    load_tile_p(tend);
+                    base = tb;
+                    continue;
+                }
+                const int q = base + lane;
+                const bool unc = q < tend && (!use_t || !(dp < (double)ts[q - tb]));
+                mask = __ballot_sync(0xffffffffu, unc);
+                if (mask) break;
+                base += 32;
+            }
+            // keep at most free_slots candidates (lowest positions first)
+            const int navail = min(__popc(mask), free_slots);
+            if (navail > 0) {
+                const unsigned lower = (lane == 0) ? 0u : (mask & ((1u << lane) - 1u));
+                const int rank = __popc(lower);
+                const bool mine = ((mask >> lane) & 1u) && rank < navail;
+                if (mine) {
+                    const int p = base + lane;
+                    const int k = k_issue + rank;
+                    const int s = k & kmask;
+                    const int32_t j = As[p - tb];
+                    const unsigned slot = ring_s + (unsigned)s * sbytes;
+                    const unsigned b = bar_s + 8u * s;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx_s(b, xbytes + (unsigned)sizeof(ColInfo));
+                    tma_bulk_g2s_s(slot + (unsigned)sizeof(SlotHdr), X + (int64_t)j * P.ld, xbytes, b);
+                    tma_bulk_g2s_s(slot, cinfo + j, (unsigned)sizeof(ColInfo), b);
+                    SlotHdr* h = reinterpret_cast<SlotHdr*>(ring + (size_t)s * sbytes);
+                    h->tcert = (double)ts[p - tb];
+                    h->dp = dp;
+                    h->pos = p;
+                    h->j = j;
+                    h->gen = gen;
+                    __threadfence_block();
+                    *(volatile int*)&cc->hdr_ready[s] = k + 1;
+                }
+                // position of the last issued candidate (rank navail-1)
+                int lastbit = 0;
+                {
+                    unsigned mm = mask;
+                    for (int r = 0; r < navail - 1; ++r) mm &= mm - 1;
+                    lastbit = __ffs(mm) - 1;
+                }
+                qnext = base + lastbit + 1;
+                k_issue += navail;
+            } else if (mask == 0 && base >= tend && tend >= m) {
+                // end of the epoch: an entry without data (plain arrive completes the phase)
+                if (lane == 0) {
+                    const int s = k_issue & kmask;
+                    SlotHdr* h = reinterpret_cast<SlotHdr*>(ring + (size_t)s * sbytes);
+                    h->pos = m;
+                    h->gen = gen;
+                    mbar_arrive_s(bar_s + 8u * s);
+                    __threadfence_block();
+                    *(volatile int*)&cc->hdr_ready[s] = k_issue + 1;
+                }
+                ++k_issue;
+                done = true;
+            }
+            __syncwarp();
+        }
+        // drain outstanding transactions before the ring memory is reused
+        while (k_data < k_issue) {
+            const int s = k_data & kmask;
+            int ok = 0;
+            if (lane == 0) ok = mbar_test_s(bar_s + 8u * s, (unsigned)((k_data >> kshift) & 1));
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (ok) ++k_data; else spin_guard(t0);
         }
     } else if (w < W) {
         // =================== compute warps ===================
@@ -701,18 +740,47 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
         ColInfo* cinfo_w = P.cinfo;
         float* tg = P.t;
         int pb = 0, gen = 0, last = -1;
-        int n_unc = 0, n_nz = 0, n_req = 0;
+        int n_unc = 0, n_nz = 0, n_req = 0, n_cand = 0, n_skip = 0;
         for (int k = 0;; ++k) {
-            const int s = k % K;
-            if (ld_vol(&cc->ready[s]) != k + 1) {
+            const int s = k & kmask;
+            if (ld_vol(&cc->hdr_ready[s]) != k + 1) {
                 const unsigned long long t0 = gtimer();
-                while (ld_vol(&cc->ready[s]) != k + 1) spin_guard(t0);
+                while (ld_vol(&cc->hdr_ready[s]) != k + 1) spin_guard(t0);
             }
             __threadfence_block();
             const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
             const int pos = h->pos;
             const int hg = h->gen;
             const double tc = h->tcert, dp = h->dp;
+            bool process = hg == gen && pos < m;
+            if (process && use_t) {
+                if (D > dp) {
+                    // drift outgrew the queue's bound: restart after the last processed position
+                    ++n_req;
+                    ++gen;
+                    if (tid == 0) { *(volatile int*)&cc->req_pos = last + 1; __threadfence_block(); *(volatile int*)&cc->req_gen = gen; }
+                    process = false;
+                } else if (D < tc) {
+                    ++n_skip;                              // certified: zero update
+                    process = false;
+                }
+            }
+            if (!process) {
+                __syncwarp();
+                if (lane == 0) { __threadfence_block(); *(volatile int*)&cc->consumed[w] = k + 1; }
+                if (hg == gen && pos >= m) {
+                    if (tid == 0) { __threadfence_block(); *(volatile int*)&cc->finished = 1; }
+                    break;
+                }
+                if (hg == gen) ++n_cand;
+                continue;
+            }
+            ++n_cand;
+            if (ld_vol(&cc->data_ready[s]) != k + 1) {
+                const unsigned long long t0 = gtimer();
+                while (ld_vol(&cc->data_ready[s]) != k + 1) spin_guard(t0);
+            }
+            __threadfence_block();
             const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
             const int32_t j = h->j;
             const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
@@ -721,21 +789,6 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
             for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
             __syncwarp();
             if (lane == 0) { __threadfence_block(); *(volatile int*)&cc->consumed[w] = k + 1; }   // slot fully read
-            if (hg != gen) continue;                                   // stale entry before a restart
-            if (pos >= m) {
-                if (tid == 0) { __threadfence_block(); *(volatile int*)&cc->finished = 1; }
-                break;
-            }
-            if (use_t) {
-                if (D > dp) {
-                    // drift outgrew the queue's bound: restart after the last processed position
-                    ++n_req;
-                    ++gen;
-                    if (tid == 0) { *(volatile int*)&cc->req_pos = last + 1; __threadfence_block(); *(volatile int*)&cc->req_gen = gen; }
-                    continue;
-                }
-                if (D < tc) continue;                                  // certified: zero update
-            }
             // ---- critical chain
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -804,6 +857,8 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
             ctl->epoch_unc = n_unc;
             ctl->epoch_nz = n_nz;
             ctl->n_requeue += n_req;
+            ctl->n_cand += n_cand;
+            ctl->n_skip += n_skip;
             P.sc->visits += (unsigned long long)m;
             P.sc->uncertified += (unsigned long long)n_unc;
             P.sc->nonzero += (unsigned long long)n_nz;
@@ -1255,6 +1310,105 @@ __global__ void __launch_bounds__(256, 1) k_screen_full(const SolveDev* __restri
     Group g{(int)gridDim.x, (int)blockIdx.x, nullptr};
     group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, 0.0, radius,
                   reinterpret_cast<double*>(smem));
+}
+
+// ---------------------------------------------------------------------------
+// Batched independent problems (BASELINE cfg4, stability selection): one CTA
+// per problem runs its whole warm-started lambda path on the device -- the
+// lambda loop, the lambda_max shortcut, the sequential screen and every solve
+// -- so problems never wait for each other (no per-lambda global barrier).
+// ---------------------------------------------------------------------------
+struct BatchOut {
+    const double* grid;     // [T] lambdas of this problem
+    double lmax;
+    double* betas;          // [T * p] or nullptr
+    int64_t* passes;        // [T]
+    double* gaps;           // [T]
+    int32_t* converged;     // [T]
+    int64_t* n_active;      // [T]
+    int T;
+};
+
+template <typename T, int R>
+__global__ void __launch_bounds__(256, 1) k_batch_path(SolveDev* probs, const BatchOut* outs) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ SolveDev sp;
+    __shared__ int sh[32];
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) sp = probs[b];
+    __syncthreads();
+    const BatchOut& o = outs[b];
+    Group g{1, 0, nullptr};
+    DevScalars* sc = sp.sc;
+    SolveCtl* ctl = sp.ctl;
+    const int64_t p = sp.p;
+    const int n = sp.n;
+    double prev_margin = 1.0;
+    int prev_interp = 0;
+    const bool gap_rule = sp.rule == 1;
+    for (int t = 0; t < o.T; ++t) {
+        const double lam = o.grid[t];
+        if (lam >= o.lmax * (1 - 1e-14)) {
+            // _solve_at_lambda_max (solver.py:129-146): beta = 0, theta = y/lam, rho = y,
+            // active = {|x_j^T theta| >= 1 - 1e-9} (rule gap) or nonzero-norm columns
+            for (int64_t j = threadIdx.x; j < p; j += blockDim.x) sp.beta[j] = 0.0;
+            for (int r = threadIdx.x; r < n; r += blockDim.x) {
+                const double y = sp.y[r];
+                sp.rho[r] = y;
+                sp.theta[r] = y / lam;
+            }
+            __syncthreads();
+            if (gap_rule) {
+                group_gemv<T>(g, sp, sp.theta, nullptr, p, G_MU, nullptr, nullptr, 0.0, 0.0, 0.0,
+                              reinterpret_cast<double*>(smem + (sp.sparse ? 0 : sp.cd_bytes)));
+            } else {
+                for (int64_t j = threadIdx.x; j < p; j += blockDim.x) sp.mark[j] = __ldg(sp.norms + j) > 0.0;
+            }
+            __syncthreads();
+            group_compact2(g, sp, p,
+                           [&](int64_t j) { return sp.mark[j] != 0; },
+                           [&](int64_t j, int64_t q) { sp.A[q] = (int32_t)j; },
+                           [&](int64_t) { return false; }, [&](int64_t, int64_t) {},
+                           &sc->m, nullptr, sh);
+            __syncthreads();
+            for (int64_t j = threadIdx.x; j < p; j += blockDim.x) sp.mark[j] = 0;
+            if (threadIdx.x == 0) {
+                o.passes[t] = 0;
+                o.gaps[t] = 0.0;
+                o.converged[t] = 1;
+                o.n_active[t] = sc->m;
+            }
+            prev_margin = 0.0;
+            prev_interp = 0;
+        } else {
+            if (threadIdx.x == 0) {
+                sp.lam = lam;
+                sp.init_mode = (gap_rule && t > 0 && !prev_interp) ? 2 : 0;
+                sp.prev_margin = prev_margin;
+                sc->lam = lam;
+                sc->status = ST_OK;
+                SolveCtl z{};
+                *ctl = z;
+            }
+            __syncthreads();
+            solve_body<T, R>(sp, g, smem);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                o.passes[t] = ctl->passes;
+                o.gaps[t] = ctl->final_done ? sc->gap_pre : sc->gap_post;
+                o.converged[t] = sc->status != ST_OK ? -1 : ctl->converged;
+                o.n_active[t] = sc->m;
+            }
+            prev_margin = sc->margin;
+            prev_interp = sc->interp;
+            if (sc->status != ST_OK) break;   // error status: stop this problem (host raises)
+        }
+        if (o.betas) {
+            double* dst = o.betas + (int64_t)t * p;
+            for (int64_t j = threadIdx.x; j < p; j += blockDim.x) dst[j] = sp.beta[j];
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace gs

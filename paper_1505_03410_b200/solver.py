@@ -209,7 +209,9 @@ class DeviceSolver:
                            device_ms=float(res.device_ms), screen_ms=float(res.screen_ms),
                            ckpt_ms=float(res.ckpt_ms), refresh_ms=float(res.refresh_ms),
                            cd_ms=float(res.cd_ms), n_screen=int(res.n_screen),
-                           n_refresh=int(res.n_refresh), launches=int(res.launches))
+                           n_refresh=int(res.n_refresh), launches=int(res.launches),
+                           cd_candidates=int(res.cd_candidates), cd_skipped=int(res.cd_skipped),
+                           cd_requeues=int(res.cd_requeues))
         return beta, cert, state
 
 
@@ -291,3 +293,61 @@ class PathTimer:
         d2h = res.betas.nbytes + sum(s.residual.nbytes + s.theta.theta.nbytes + s.active.nbytes
                                      for s in res.states)
         return best, int(h2d), int(d2h)
+
+
+class BatchPathSolver:
+    """Independent Lasso paths on row-resampled copies of one design
+    (BASELINE configs[4], stability selection).  Problem b uses rows
+    ``rows[b]`` (with repetition) of ``X0`` and of ``y0``.  All problems run
+    concurrently, one CTA each, with the whole warm-started lambda path on the
+    device (no per-lambda synchronisation between problems)."""
+
+    def __init__(self, X0, y0: np.ndarray, rows: np.ndarray):
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        if rows.ndim != 2:
+            raise ValueError("rows must be (B, n)")
+        self.B, self.n = rows.shape
+        self.p = X0.n_cols
+        self._lib = X0._lib
+        y0 = np.ascontiguousarray(y0, dtype=np.float64)
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.gs_batch_create(X0.handle, _lib.f64p(y0), _lib.i32p(rows), self.B, self.n,
+                                             ctypes.byref(h)))
+        self._h = h
+        lm = np.empty(self.B)
+        _lib.check(self._lib.gs_batch_lambda_max(h, _lib.f64p(lm)))
+        self.lambda_max = lm
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.gs_batch_free(h)
+            self._h = None
+
+    def run_paths(self, grids: np.ndarray, config: SolverConfig, want_betas: bool = False):
+        """grids: (B, T) non-increasing per row.  Returns a dict of (B, T)
+        arrays: passes, gaps, converged, n_active (+ betas (B, T, p)) and the
+        device time in ms."""
+        if config.rule not in _GPU_RULES:
+            raise NotImplementedError(f"rule {config.rule.value!r} is not on the B200 path in this build")
+        grids = np.ascontiguousarray(grids, dtype=np.float64)
+        B, T = grids.shape
+        if B != self.B:
+            raise ValueError("grids must have one row per problem")
+        if np.any(np.diff(grids, axis=1) > 0):
+            raise ValueError("grid must be non-increasing")
+        cfg = _lib.SolveConfig(float(config.epsilon), int(config.max_passes), int(config.screen_every),
+                               _GPU_RULES[config.rule], int(bool(config.certify)), _lib.CKPT_CB(), None)
+        passes = np.empty((B, T), dtype=np.int64)
+        gaps = np.empty((B, T))
+        conv = np.empty((B, T), dtype=np.int32)
+        nact = np.empty((B, T), dtype=np.int64)
+        betas = np.empty((B, T, self.p)) if want_betas else None
+        ms = ctypes.c_double()
+        _lib.check(self._lib.gs_batch_run_paths(self._h, _lib.f64p(grids), T, ctypes.byref(cfg),
+                                                _lib.f64p(betas), _lib.i64p(passes), _lib.f64p(gaps),
+                                                _lib.i32p(conv), _lib.i64p(nact), ctypes.byref(ms)))
+        out = dict(passes=passes, gaps=gaps, converged=conv.astype(bool), n_active=nact, device_ms=ms.value)
+        if want_betas:
+            out["betas"] = betas
+        return out

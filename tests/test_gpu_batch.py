@@ -1,0 +1,42 @@
+"""Batched independent problems (BASELINE configs[4]): every problem's
+device-side path equals the oracle's run_path on the same resampled rows."""
+
+import numpy as np
+import pytest
+
+from oracle import gapsafe_oracle as O
+from paper_1505_03410_b200 import synth
+from parity import beta_close, gap_close
+
+gs = pytest.importorskip("paper_1505_03410_b200")
+pytestmark = pytest.mark.gpu
+
+
+def test_batch_paths_match_oracle():
+    rng = np.random.default_rng(11)
+    X0 = synth.ar1_design(rng, 300, 1500, 0.5)
+    beta = np.zeros(1500)
+    beta[rng.choice(1500, 15, replace=False)] = rng.choice([-1.0, 1.0], 15)
+    y0 = X0 @ beta + 0.3 * rng.standard_normal(300)
+    B, n, T = 6, 150, 12
+    rows = np.stack([np.random.default_rng([4, b]).integers(0, 300, n) for b in range(B)]).astype(np.int32)
+    D0 = gs.DesignMatrix(X0)
+    bs = gs.BatchPathSolver(D0, y0, rows)
+    grids = np.stack([gs.lambda_grid(bs.lambda_max[b], T, 2.0) for b in range(B)])
+    eps = np.array([1e-8 * float(y0[rows[b]] @ y0[rows[b]]) for b in range(B)])
+    # one epsilon per run: use the smallest (all problems solved at least that tightly)
+    res = bs.run_paths(grids, gs.SolverConfig(epsilon=float(eps.min()), max_passes=100_000), want_betas=True)
+    for b in range(B):
+        Xb = np.asfortranarray(X0[rows[b]])
+        yb = y0[rows[b]]
+        ref = O.run_path(O.DesignMatrix(Xb), yb, grids[b],
+                         O.SolverConfig(epsilon=float(eps.min()), max_passes=100_000))
+        yy = float(yb @ yb)
+        for t in range(T):
+            st = ref.states[t]
+            assert res["passes"][b, t] == st.passes_done, (b, t)
+            assert res["converged"][b, t] == st.converged
+            assert res["n_active"][b, t] == st.active.size, (b, t)
+            assert np.array_equal(np.flatnonzero(res["betas"][b, t]), np.flatnonzero(st.beta)), (b, t)
+            assert beta_close(res["betas"][b, t], st.beta), (b, t)
+            assert gap_close(res["gaps"][b, t], st.cert.gap, yy), (b, t)

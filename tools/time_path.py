@@ -30,5 +30,8 @@ out = dict(config=name, upload_s=t1 - t0, path_s_first=t2 - t1, path_s=t3 - t2,
            device_ms=float(sum(x["device_ms"] for x in st)),
            phase_ms={k: float(sum(x[k] for x in st)) for k in ("screen_ms", "ckpt_ms", "refresh_ms", "cd_ms")},
            refreshes=int(sum(x["n_refresh"] for x in st)),
+           candidates=int(sum(x["cd_candidates"] for x in st)),
+           skipped=int(sum(x["cd_skipped"] for x in st)),
+           requeues=int(sum(x["cd_requeues"] for x in st)),
            converged=int(res.converged.sum()))
 print(json.dumps(out))
