@@ -211,7 +211,7 @@ def run_ours(args):
     inpath_screen = agg["screen_ms"] / max(1, agg["n_screen"])
 
     # ---- e2e through the public API from pinned host buffers
-    e2e_ms, h2d, d2h = timer.e2e_path_ms(case, grid, cfg, reps=max(1, min(args.steps, 2)))
+    e2e_ms, h2d, d2h = timer.e2e_path_ms(case, grid, cfg, reps=1)
 
     line = {
         "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,

@@ -19,6 +19,8 @@
 #pragma once
 #include "gs_kernels.cuh"
 
+#include <cstdio>
+
 namespace gs {
 
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -504,9 +506,16 @@ struct alignas(16) CdCtl {
     int finished, pad0, pad1, pad2;       // compute warps consumed the current-generation end entry
 };
 
-// bounded spin: a protocol error traps (launch failure) instead of hanging the GPU
-__device__ __forceinline__ void spin_guard(unsigned long long t0) {
-    if (gtimer() - t0 > 20000000000ull) __trap();
+// bounded spin: a protocol error traps (launch failure) instead of hanging the
+// GPU; the message names the wait and the queue state
+__device__ __noinline__ void spin_fail(int where, int a, int b, int c, int d) {
+    printf("gapsafe_b200 watchdog: wait %d expired (block %d thread %d: %d %d %d %d)\n", where, (int)blockIdx.x,
+           (int)threadIdx.x, a, b, c, d);
+    __trap();
+}
+__device__ __forceinline__ void spin_guard(unsigned long long t0, int where = 0, int a = 0, int b = 0, int c = 0,
+                                           int d = 0) {
+    if (gtimer() - t0 > 20000000000ull) spin_fail(where, a, b, c, d);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -531,6 +540,16 @@ __device__ __forceinline__ void tma_bulk_g2s_s(unsigned dst, const void* src, un
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(b) : "memory");
 }
 __device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
+// CTA-scope acquire load / release store on shared memory (the load is a
+// plain LDS on sm_100a; the store is MEMBAR.ALL.CTA + STS)
+__device__ __forceinline__ int ld_acq(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel(int* p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 
 // first position in [from, lim) with !(D < t) (uncertified under D)
 __device__ __forceinline__ int scan_under(const float* ts, int tb, int lim, int from, double D, int lane) {
@@ -620,13 +639,15 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
             for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
             __syncwarp();
         };
-        while (!ld_vol(&cc->finished)) {
+        // every control word is read by lane 0 and broadcast: the warp must take
+        // uniform decisions (ballots and shuffles below use the full mask)
+        auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
+        while (!bcast(lane == 0 ? ld_acq(&cc->finished) : 0)) {
             // restart request from the compute warps
-            const int rg = ld_vol(&cc->req_gen);
+            const int rg = bcast(lane == 0 ? ld_acq(&cc->req_gen) : 0);
             if (rg != gen) {
-                __threadfence_block();
                 gen = rg;
-                const int rp = ld_vol(&cc->req_pos);
+                const int rp = bcast(lane == 0 ? ld_acq(&cc->req_pos) : 0);
                 if (rp < tb || rp > tend || (rp == tend && tend < m)) load_tile_p(rp);
                 qnext = rp;
                 done = false;
@@ -638,22 +659,25 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
                 if (lane == 0) ok = mbar_test_s(bar_s + 8u * s, (unsigned)((k_data >> kshift) & 1));
                 ok = __shfl_sync(0xffffffffu, ok, 0);
                 if (!ok) break;
-                if (lane == 0) { __threadfence_block(); *(volatile int*)&cc->data_ready[s] = k_data + 1; }
+                if (lane == 0) st_rel(&cc->data_ready[s], k_data + 1);
                 ++k_data;
                 t0 = gtimer();
             }
             // free slots: entries consumed by every compute warp and whose bytes landed
             int cmin = 0x7fffffff;
-            for (int q = 0; q < W; ++q) cmin = min(cmin, ld_vol(&cc->consumed[q]));
+            if (lane == 0)
+                for (int q = 0; q < W; ++q) cmin = min(cmin, ld_acq(&cc->consumed[q]));
+            cmin = bcast(cmin);
             const int free_slots = min(K - (k_issue - cmin), K - (k_issue - k_data));
             if (done || free_slots <= 0) {
                 __nanosleep(32);
-                spin_guard(t0);
+                spin_guard(t0, 1, k_issue, k_data, cmin, (int)done);
                 continue;
             }
-            __threadfence_block();
             // one ballot: every candidate of the next window
-            const double dp = use_t ? __dadd_ru(*(const volatile double*)&cc->dpub, margin_gs) : 0.0;
+            double dpub = lane == 0 ? *(const volatile double*)&cc->dpub : 0.0;
+            dpub = __shfl_sync(0xffffffffu, dpub, 0);
+            const double dp = use_t ? __dadd_ru(dpub, margin_gs) : 0.0;
             int base = qnext;
             unsigned mask = 0;
             while (true) {
@@ -692,8 +716,7 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
                     h->pos = p;
                     h->j = j;
                     h->gen = gen;
-                    __threadfence_block();
-                    *(volatile int*)&cc->hdr_ready[s] = k + 1;
+                    st_rel(&cc->hdr_ready[s], k + 1);
                 }
                 // position of the last issued candidate (rank navail-1)
                 int lastbit = 0;
@@ -712,8 +735,7 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
                     h->pos = m;
                     h->gen = gen;
                     mbar_arrive_s(bar_s + 8u * s);
-                    __threadfence_block();
-                    *(volatile int*)&cc->hdr_ready[s] = k_issue + 1;
+                    st_rel(&cc->hdr_ready[s], k_issue + 1);
                 }
                 ++k_issue;
                 done = true;
@@ -726,7 +748,7 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
             int ok = 0;
             if (lane == 0) ok = mbar_test_s(bar_s + 8u * s, (unsigned)((k_data >> kshift) & 1));
             ok = __shfl_sync(0xffffffffu, ok, 0);
-            if (ok) ++k_data; else spin_guard(t0);
+            if (ok) ++k_data; else spin_guard(t0, 2, k_issue, k_data, 0, 0);
         }
     } else if (w < W) {
         // =================== compute warps ===================
@@ -741,13 +763,13 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
         float* tg = P.t;
         int pb = 0, gen = 0, last = -1;
         int n_unc = 0, n_nz = 0, n_req = 0, n_cand = 0, n_skip = 0;
+        const int cmask = min(7, (K >> 2) - 1);     // consumed is signalled every cmask+1 entries
         for (int k = 0;; ++k) {
             const int s = k & kmask;
-            if (ld_vol(&cc->hdr_ready[s]) != k + 1) {
+            if (ld_acq(&cc->hdr_ready[s]) != k + 1) {
                 const unsigned long long t0 = gtimer();
-                while (ld_vol(&cc->hdr_ready[s]) != k + 1) spin_guard(t0);
+                while (ld_acq(&cc->hdr_ready[s]) != k + 1) spin_guard(t0, 3, k, ld_acq(&cc->hdr_ready[s]), gen, last);
             }
-            __threadfence_block();
             const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
             const int pos = h->pos;
             const int hg = h->gen;
@@ -758,7 +780,7 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
                     // drift outgrew the queue's bound: restart after the last processed position
                     ++n_req;
                     ++gen;
-                    if (tid == 0) { *(volatile int*)&cc->req_pos = last + 1; __threadfence_block(); *(volatile int*)&cc->req_gen = gen; }
+                    if (tid == 0) { *(volatile int*)&cc->req_pos = last + 1; st_rel(&cc->req_gen, gen); }
                     process = false;
                 } else if (D < tc) {
                     ++n_skip;                              // certified: zero update
@@ -766,29 +788,27 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
                 }
             }
             if (!process) {
-                __syncwarp();
-                if (lane == 0) { __threadfence_block(); *(volatile int*)&cc->consumed[w] = k + 1; }
+                // consumed is signalled in batches of 8 entries (release store)
+                if ((k & cmask) == cmask) { __syncwarp(); if (lane == 0) st_rel(&cc->consumed[w], k + 1); }
                 if (hg == gen && pos >= m) {
-                    if (tid == 0) { __threadfence_block(); *(volatile int*)&cc->finished = 1; }
+                    if (tid == 0) st_rel(&cc->finished, 1);
                     break;
                 }
                 if (hg == gen) ++n_cand;
                 continue;
             }
             ++n_cand;
-            if (ld_vol(&cc->data_ready[s]) != k + 1) {
+            if (ld_acq(&cc->data_ready[s]) != k + 1) {
                 const unsigned long long t0 = gtimer();
-                while (ld_vol(&cc->data_ready[s]) != k + 1) spin_guard(t0);
+                while (ld_acq(&cc->data_ready[s]) != k + 1) spin_guard(t0, 4, k, ld_acq(&cc->data_ready[s]), gen, last);
             }
-            __threadfence_block();
             const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
             const int32_t j = h->j;
             const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
             double xv[R];
 #pragma unroll
             for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
-            __syncwarp();
-            if (lane == 0) { __threadfence_block(); *(volatile int*)&cc->consumed[w] = k + 1; }   // slot fully read
+            if ((k & cmask) == cmask) { __syncwarp(); if (lane == 0) st_rel(&cc->consumed[w], k + 1); }   // slots fully read
             // ---- critical chain
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll

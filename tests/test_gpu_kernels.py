@@ -201,3 +201,30 @@ def test_screen_matches_oracle(sparse):
         diff = np.setxor1d(a.active_set, b.active_set)
         assert np.all(near[diff])
         np.testing.assert_allclose(a.mu, b.mu, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("n", [40, 72, 200, 384, 640, 1000, 1500])
+def test_cd_pipeline_stress(n):
+    """Many epochs of the warp-specialized CD (all warp-group sizes and ring
+    depths, several active-set sizes incl. multi-tile) against the sequential
+    reference; a protocol hang would trip the device watchdog and raise."""
+    rng = np.random.default_rng(n)
+    p = 9000 if n <= 72 else 2500
+    X = np.asfortranarray(rng.standard_normal((n, p)))
+    X /= np.linalg.norm(X, axis=0)
+    X = np.asfortranarray(X)
+    y = X[:, :12] @ rng.standard_normal(12) + 0.1 * rng.standard_normal(n)
+    nsq = np.einsum("ij,ij->j", X, X)
+    D = gs.DesignMatrix(X)
+    for lam_frac in (0.5, 0.1, 0.02):
+        lam = lam_frac * np.max(np.abs(X.T @ y))
+        active = np.arange(p, dtype=np.int64)
+        b_ref, r_ref = np.zeros(p), y.copy()
+        st = gs.SolverState(beta=np.zeros(p), residual=y.copy(), active=active, theta=None, cert=None,
+                            passes_done=0, converged=False)
+        prob = gs.LassoProblem(D, y, lam)
+        for _ in range(4):
+            O.cd_pass_dense(X, b_ref, r_ref, active, lam, nsq, 0.0)
+            gs.cd_pass(st, prob)
+        assert np.array_equal(np.flatnonzero(st.beta), np.flatnonzero(b_ref))
+        np.testing.assert_allclose(st.beta, b_ref, rtol=0, atol=1e-10 * max(1, np.abs(b_ref).max()))
