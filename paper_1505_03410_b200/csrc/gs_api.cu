@@ -4,6 +4,7 @@
 // include/gapsafe_b200.h.
 #include "../../include/gapsafe_b200.h"
 #include "gs_solve.cuh"
+#include "gs_launch.h"
 
 #include <cmath>
 #include <cstdlib>
@@ -493,60 +494,19 @@ static CdShape cd_shape(int64_t n) {
     return {0, 0};
 }
 
-template <typename T, int R>
-static int launch_solve_T(cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem) {
-    auto kern = k_solve<T, R>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int G_ = G;
-    void* args[] = {(void*)&dprobs, (void*)&G_};
-    COUNT_LAUNCH(1);
-    CK(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)(G * nprob)), dim3(kSolveThreads), args, smem, st));
-    return GS_OK;
-}
-
 static int launch_solve(const gs_matrix* M, cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem,
                         int R) {
-    if (M->sparse || M->dtype == GS_DTYPE_F64) {
-        switch (R) {
-            case 1: return launch_solve_T<double, 1>(st, dprobs, G, nprob, smem);
-            case 2: return launch_solve_T<double, 2>(st, dprobs, G, nprob, smem);
-            case 4: return launch_solve_T<double, 4>(st, dprobs, G, nprob, smem);
-            default: return launch_solve_T<double, 8>(st, dprobs, G, nprob, smem);
-        }
-    }
-    switch (R) {
-        case 1: return launch_solve_T<float, 1>(st, dprobs, G, nprob, smem);
-        case 2: return launch_solve_T<float, 2>(st, dprobs, G, nprob, smem);
-        case 4: return launch_solve_T<float, 4>(st, dprobs, G, nprob, smem);
-        default: return launch_solve_T<float, 8>(st, dprobs, G, nprob, smem);
-    }
-}
-
-template <typename T, int R>
-static int launch_cdpass_T(cudaStream_t st, const SolveDev* dprobs, size_t smem) {
-    auto kern = k_cd_pass_prod<T, R>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const bool f64 = M->sparse || M->dtype == GS_DTYPE_F64;
     COUNT_LAUNCH(1);
-    kern<<<1, kSolveThreads, smem, st>>>(dprobs);
-    CKL();
+    CK(f64 ? gs_launch_solve_f64(R, st, dprobs, G, nprob, smem) : gs_launch_solve_f32(R, st, dprobs, G, nprob, smem));
     return GS_OK;
 }
 
 static int launch_cdpass(const gs_matrix* M, cudaStream_t st, const SolveDev* dprobs, size_t smem, int R) {
-    if (M->sparse || M->dtype == GS_DTYPE_F64) {
-        switch (R) {
-            case 1: return launch_cdpass_T<double, 1>(st, dprobs, smem);
-            case 2: return launch_cdpass_T<double, 2>(st, dprobs, smem);
-            case 4: return launch_cdpass_T<double, 4>(st, dprobs, smem);
-            default: return launch_cdpass_T<double, 8>(st, dprobs, smem);
-        }
-    }
-    switch (R) {
-        case 1: return launch_cdpass_T<float, 1>(st, dprobs, smem);
-        case 2: return launch_cdpass_T<float, 2>(st, dprobs, smem);
-        case 4: return launch_cdpass_T<float, 4>(st, dprobs, smem);
-        default: return launch_cdpass_T<float, 8>(st, dprobs, smem);
-    }
+    const bool f64 = M->sparse || M->dtype == GS_DTYPE_F64;
+    COUNT_LAUNCH(1);
+    CK(f64 ? gs_launch_cdpass_f64(R, st, dprobs, smem) : gs_launch_cdpass_f32(R, st, dprobs, smem));
+    return GS_OK;
 }
 
 static int vs_cap_for(const gs_matrix* M) { return M->sparse ? 24576 : 6144; }
@@ -1066,7 +1026,7 @@ extern "C" int gs_screen_timed(const gs_matrix* M, const double* center, double 
     d.X = M->X; d.ld = M->ld; d.n = (int)M->n; d.dtype = M->dtype; d.p = M->p; d.sparse = M->sparse;
     d.data = M->data; d.indices = M->indices; d.indptr = M->indptr; d.norms = M->norms; d.nsq = M->norms_sq;
     d.inv_nsq = M->inv_nsq;
-    d.theta = dv; d.mark = mark; d.vs_cap = vs_cap_for(M);
+    d.theta = dv; d.mark = mark; d.vs_cap = vs_cap_for(M); d.cd_bytes = (int)cd_bytes_for(M);
     CK(cudaMemcpyAsync(dp, &d, sizeof d, cudaMemcpyHostToDevice, st));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1078,13 +1038,9 @@ extern "C" int gs_screen_timed(const gs_matrix* M, const double* center, double 
     CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
     int rc = GS_OK;
     const bool f64 = M->sparse || M->dtype == GS_DTYPE_F64;
-    if (f64) CK(cudaFuncSetAttribute(k_screen_full<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    else CK(cudaFuncSetAttribute(k_screen_full<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     auto gemv = [&]() -> int {
         COUNT_LAUNCH(1);
-        if (f64) k_screen_full<double><<<sms, kSolveThreads, smem, st>>>(dp, radius);
-        else k_screen_full<float><<<sms, kSolveThreads, smem, st>>>(dp, radius);
-        CKL();
+        CK(f64 ? gs_launch_screen_full_f64(st, dp, radius, sms, smem) : gs_launch_screen_full_f32(st, dp, radius, sms, smem));
         return GS_OK;
     };
     // warm-up pass (GEMV + compaction), then `reps` GEMV launches timed with
@@ -1330,19 +1286,8 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
     CK(cudaEventRecord(e0, st));
     COUNT_LAUNCH(1);
     const bool f64 = Bt->dtype == GS_DTYPE_F64;
-#define GS_BATCH_LAUNCH(TT, RR)                                                                          \
-    do {                                                                                                  \
-        CK(cudaFuncSetAttribute(k_batch_path<TT, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        k_batch_path<TT, RR><<<(unsigned)B, kSolveThreads, smem, st>>>(Bt->dprobs, Bt->douts);           \
-    } while (0)
-    if (f64) {
-        switch (cs.R) { case 1: GS_BATCH_LAUNCH(double, 1); break; case 2: GS_BATCH_LAUNCH(double, 2); break;
-                        case 4: GS_BATCH_LAUNCH(double, 4); break; default: GS_BATCH_LAUNCH(double, 8); }
-    } else {
-        switch (cs.R) { case 1: GS_BATCH_LAUNCH(float, 1); break; case 2: GS_BATCH_LAUNCH(float, 2); break;
-                        case 4: GS_BATCH_LAUNCH(float, 4); break; default: GS_BATCH_LAUNCH(float, 8); }
-    }
-#undef GS_BATCH_LAUNCH
+CK(f64 ? gs_launch_batch_f64(cs.R, st, Bt->dprobs, Bt->douts, (int)B, smem)
+        : gs_launch_batch_f32(cs.R, st, Bt->dprobs, Bt->douts, (int)B, smem));
     CKL();
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));

@@ -171,6 +171,54 @@ template <> struct ColDot2<float> {
     }
 };
 
+// one column out of shared memory; per-lane partition, accumulation order and
+// butterfly identical to ColDot2 (bit-identical results)
+template <typename T> struct ColDotS;
+
+template <> struct ColDotS<double> {
+    static __device__ __forceinline__ double run(const double* x, const double* v, int n, int lane) {
+        const double2* p = reinterpret_cast<const double2*>(x);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const int n2 = n >> 1;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n2; q += kWarp) {
+            const double2 xa = p[q];
+            const double2 vv = v2[q];
+            a0 = fma(xa.x, vv.x, a0);
+            a1 = fma(xa.y, vv.y, a1);
+        }
+        if ((n & 1) && lane == 0) a0 = fma(x[n - 1], v[n - 1], a0);
+        double s = a0 + a1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        return s;
+    }
+};
+
+template <> struct ColDotS<float> {
+    static __device__ __forceinline__ double run(const float* x, const double* v, int n, int lane) {
+        const float4* p = reinterpret_cast<const float4*>(x);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const int n4 = n >> 2;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n4; q += kWarp) {
+            const float4 xa = p[q];
+            const double2 va = v2[2 * q], vb = v2[2 * q + 1];
+            a0 = fma((double)xa.x, va.x, a0);
+            a1 = fma((double)xa.y, va.y, a1);
+            a0 = fma((double)xa.z, vb.x, a0);
+            a1 = fma((double)xa.w, vb.y, a1);
+        }
+        for (int r = (n4 << 2) + lane; r < n; r += kWarp) a0 = fma((double)x[r], v[r], a0);
+        double s = a0 + a1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        return s;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // screening / restricted GEMV with fused epilogues
 // ---------------------------------------------------------------------------
@@ -223,7 +271,7 @@ __device__ __forceinline__ double cert_threshold(double c, double norm, double l
 }
 
 template <typename T, bool VSMEM>
-__global__ void __launch_bounds__(256) k_gemv_t_dense(const T* __restrict__ X, GemvArgs a) {
+static __global__ void __launch_bounds__(256) k_gemv_t_dense(const T* __restrict__ X, GemvArgs a) {
     extern __shared__ double smem_v[];
     __shared__ double s_val[8];
     __shared__ int64_t s_idx[8];
@@ -272,7 +320,7 @@ __global__ void __launch_bounds__(256) k_gemv_t_dense(const T* __restrict__ X, G
 }
 
 // CSC: warp per column, entries in storage order (sorted rows).
-__global__ void __launch_bounds__(256) k_gemv_t_csc(const double* __restrict__ data,
+static __global__ void __launch_bounds__(256) k_gemv_t_csc(const double* __restrict__ data,
                                                     const int32_t* __restrict__ indices,
                                                     const int64_t* __restrict__ indptr, GemvArgs a) {
     __shared__ double s_val[8];
@@ -315,7 +363,7 @@ __global__ void __launch_bounds__(256) k_gemv_t_csc(const double* __restrict__ d
 }
 
 // second stage of the block max: one block; writes (max, position) to out.
-__global__ void k_max_finalize(const double* __restrict__ bv, const int64_t* __restrict__ bi,
+static __global__ void k_max_finalize(const double* __restrict__ bv, const int64_t* __restrict__ bi,
                                int64_t nb, double* out_val, int64_t* out_idx) {
     __shared__ double s_val[32];
     __shared__ int64_t s_idx[32];
@@ -364,7 +412,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
     return excl;
 }
 
-__global__ void __launch_bounds__(256) k_compact_count(const uint8_t* __restrict__ flags, int64_t m,
+static __global__ void __launch_bounds__(256) k_compact_count(const uint8_t* __restrict__ flags, int64_t m,
                                                        int32_t* __restrict__ cnt) {
     __shared__ int sh[32];
     const int64_t base = (int64_t)blockIdx.x * kCompactChunk + threadIdx.x * 4;
@@ -377,7 +425,7 @@ __global__ void __launch_bounds__(256) k_compact_count(const uint8_t* __restrict
 }
 
 // exclusive scan of block counts (one block), writes offsets and total.
-__global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t nb, int64_t* __restrict__ off,
+static __global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t nb, int64_t* __restrict__ off,
                               int64_t* total_out) {
     __shared__ int64_t sh[1024];
     const int t = threadIdx.x, T = blockDim.x;
@@ -398,7 +446,7 @@ __global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t nb, int64
 }
 
 // out[off + rank] = cols ? cols[i] : i, for flagged i in ascending order.
-__global__ void __launch_bounds__(256) k_compact_scatter(const uint8_t* __restrict__ flags, int64_t m,
+static __global__ void __launch_bounds__(256) k_compact_scatter(const uint8_t* __restrict__ flags, int64_t m,
                                                          const int32_t* __restrict__ cols,
                                                          const int64_t* __restrict__ off,
                                                          int32_t* __restrict__ out) {
@@ -418,7 +466,7 @@ __global__ void __launch_bounds__(256) k_compact_scatter(const uint8_t* __restri
 // ---------------------------------------------------------------------------
 // small element-wise kernels
 // ---------------------------------------------------------------------------
-__global__ void k_flags_norm_pos(const int32_t* __restrict__ cols, int64_t m, const double* __restrict__ norms,
+static __global__ void k_flags_norm_pos(const int32_t* __restrict__ cols, int64_t m, const double* __restrict__ norms,
                                  uint8_t* __restrict__ flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = cols ? cols[i] : i;
@@ -426,7 +474,7 @@ __global__ void k_flags_norm_pos(const int32_t* __restrict__ cols, int64_t m, co
     }
 }
 
-__global__ void k_flags_beta_nz(const int32_t* __restrict__ cols, int64_t m, const double* __restrict__ beta,
+static __global__ void k_flags_beta_nz(const int32_t* __restrict__ cols, int64_t m, const double* __restrict__ beta,
                                 uint8_t* __restrict__ flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = cols ? cols[i] : i;
@@ -434,20 +482,20 @@ __global__ void k_flags_beta_nz(const int32_t* __restrict__ cols, int64_t m, con
     }
 }
 
-__global__ void k_set_mark(const int32_t* __restrict__ cols, int64_t m, uint8_t* __restrict__ mark) {
+static __global__ void k_set_mark(const int32_t* __restrict__ cols, int64_t m, uint8_t* __restrict__ mark) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         mark[cols[i]] = 1;
 }
 
 // beta_j = 0 where mark_j == 0 (solver.py:176-178), then clears mark.
-__global__ void k_zero_unmarked(double* __restrict__ beta, uint8_t* __restrict__ mark, int64_t p) {
+static __global__ void k_zero_unmarked(double* __restrict__ beta, uint8_t* __restrict__ mark, int64_t p) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
         if (!mark[j]) beta[j] = 0.0;
         mark[j] = 0;
     }
 }
 
-__global__ void k_scale_vec(const double* __restrict__ x, double s, int64_t n, double* __restrict__ out,
+static __global__ void k_scale_vec(const double* __restrict__ x, double s, int64_t n, double* __restrict__ out,
                             int divide) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = divide ? x[i] / s : x[i] * s;
@@ -458,7 +506,7 @@ __global__ void k_scale_vec(const double* __restrict__ x, double s, int64_t n, d
 // ---------------------------------------------------------------------------
 // partial[c*n + r] = sum_{k in chunk c} X[r, S[k]] * beta[S[k]]  (ascending k, FMA)
 template <typename T>
-__global__ void __launch_bounds__(256) k_resync_partial_dense(const T* __restrict__ X, int64_t ld, int n,
+static __global__ void __launch_bounds__(256) k_resync_partial_dense(const T* __restrict__ X, int64_t ld, int n,
                                                               const int32_t* __restrict__ S,
                                                               const int64_t* __restrict__ s_count,
                                                               const double* __restrict__ beta, int nchunks,
@@ -478,7 +526,7 @@ __global__ void __launch_bounds__(256) k_resync_partial_dense(const T* __restric
 }
 
 // out[r] = (y ? y[r] - sum : sum) over chunks in ascending order.
-__global__ void k_resync_final(const double* __restrict__ y, const double* __restrict__ partial, int nchunks,
+static __global__ void k_resync_final(const double* __restrict__ y, const double* __restrict__ partial, int nchunks,
                                int n, double* __restrict__ out) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
@@ -488,7 +536,7 @@ __global__ void k_resync_final(const double* __restrict__ y, const double* __res
 }
 
 // CSR row products: out[r] = (y ? y[r] - sum : sum), sum over the row in column order.
-__global__ void k_resync_csr(const double* __restrict__ data, const int32_t* __restrict__ cols,
+static __global__ void k_resync_csr(const double* __restrict__ data, const int32_t* __restrict__ cols,
                              const int64_t* __restrict__ rowptr, int n, const double* __restrict__ beta,
                              const double* __restrict__ y, double* __restrict__ out) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -501,7 +549,7 @@ __global__ void k_resync_csr(const double* __restrict__ data, const int32_t* __r
 // rho += beta_j x_j for dropped j in ascending order (numpy: v += a * x,
 // separate roundings), thread per row.
 template <typename T>
-__global__ void k_drop_axpy_dense(const T* __restrict__ X, int64_t ld, int n, const int32_t* __restrict__ D,
+static __global__ void k_drop_axpy_dense(const T* __restrict__ X, int64_t ld, int n, const int32_t* __restrict__ D,
                                   const int64_t* __restrict__ d_count, const double* __restrict__ beta,
                                   double* __restrict__ rho) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -517,7 +565,7 @@ __global__ void k_drop_axpy_dense(const T* __restrict__ X, int64_t ld, int n, co
 
 // CSC variant: one block, columns in ascending order, a barrier between
 // columns (rows inside one column are distinct).
-__global__ void k_drop_axpy_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
+static __global__ void k_drop_axpy_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
                                 const int64_t* __restrict__ indptr, const int32_t* __restrict__ D,
                                 const int64_t* __restrict__ d_count, const double* __restrict__ beta,
                                 double* __restrict__ rho) {
@@ -533,7 +581,7 @@ __global__ void k_drop_axpy_csc(const double* __restrict__ data, const int32_t* 
 
 // generic dot / abs-sum over device vectors (problem.py scalar algebra for
 // the drop-in helper functions).  out[0] = sum a*b, out[1] = sum |a|.
-__global__ void __launch_bounds__(1024) k_vec_stats(const double* __restrict__ a, const double* __restrict__ b,
+static __global__ void __launch_bounds__(1024) k_vec_stats(const double* __restrict__ a, const double* __restrict__ b,
                                                     int64_t n, double* out) {
     __shared__ double red[32];
     double s = 0.0, t = 0.0;
@@ -551,7 +599,7 @@ __global__ void __launch_bounds__(1024) k_vec_stats(const double* __restrict__ a
 // exact-order kernel twins (reference summation order, for bit-exact tests)
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void k_tdot_exact_dense(const T* __restrict__ X, int64_t ld, int n, const double* __restrict__ v,
+static __global__ void k_tdot_exact_dense(const T* __restrict__ X, int64_t ld, int n, const double* __restrict__ v,
                                    const int32_t* __restrict__ cols, int64_t k, double tail_scale,
                                    double* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
@@ -564,7 +612,7 @@ __global__ void k_tdot_exact_dense(const T* __restrict__ X, int64_t ld, int n, c
     }
 }
 
-__global__ void k_tdot_exact_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
+static __global__ void k_tdot_exact_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
                                  const int64_t* __restrict__ indptr, int n, const double* __restrict__ v,
                                  const int32_t* __restrict__ cols, int64_t k, double tail_scale,
                                  double* __restrict__ out) {
@@ -580,7 +628,7 @@ __global__ void k_tdot_exact_csc(const double* __restrict__ data, const int32_t*
 // one block: thread 0 forms the sequential non-FMA dot, all threads apply the
 // axpy with separate roundings (_kernels.py:39-92 arithmetic, bit for bit).
 template <typename T>
-__global__ void k_cd_pass_exact_dense(const T* __restrict__ X, int64_t ld, int n, double* __restrict__ beta,
+static __global__ void k_cd_pass_exact_dense(const T* __restrict__ X, int64_t ld, int n, double* __restrict__ beta,
                                       double* __restrict__ rho, const int32_t* __restrict__ A, int64_t k,
                                       double lam, const double* __restrict__ nsq, double tail_scale) {
     __shared__ double s_d;
@@ -608,7 +656,7 @@ __global__ void k_cd_pass_exact_dense(const T* __restrict__ X, int64_t ld, int n
     }
 }
 
-__global__ void k_cd_pass_exact_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
+static __global__ void k_cd_pass_exact_csc(const double* __restrict__ data, const int32_t* __restrict__ indices,
                                     const int64_t* __restrict__ indptr, int n, double* __restrict__ beta,
                                     double* __restrict__ rho, const int32_t* __restrict__ A, int64_t k, double lam,
                                     const double* __restrict__ nsq, double tail_scale) {
@@ -640,7 +688,7 @@ __global__ void k_cd_pass_exact_csc(const double* __restrict__ data, const int32
 
 // column norms: warp per column, FMA, ascending rows per lane then butterfly.
 template <typename T>
-__global__ void __launch_bounds__(256) k_col_norms_sq_dense(const T* __restrict__ X, int64_t ld, int n, int64_t p,
+static __global__ void __launch_bounds__(256) k_col_norms_sq_dense(const T* __restrict__ X, int64_t ld, int n, int64_t p,
                                                             double* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -654,7 +702,7 @@ __global__ void __launch_bounds__(256) k_col_norms_sq_dense(const T* __restrict_
     }
 }
 
-__global__ void __launch_bounds__(256) k_col_norms_sq_csc(const double* __restrict__ data,
+static __global__ void __launch_bounds__(256) k_col_norms_sq_csc(const double* __restrict__ data,
                                                           const int64_t* __restrict__ indptr, int64_t p,
                                                           double* __restrict__ out) {
     const int lane = threadIdx.x & 31;
@@ -668,7 +716,7 @@ __global__ void __launch_bounds__(256) k_col_norms_sq_csc(const double* __restri
     }
 }
 
-__global__ void k_sqrt_vec(const double* __restrict__ a, double add, int64_t p, double* __restrict__ out_sq,
+static __global__ void k_sqrt_vec(const double* __restrict__ a, double add, int64_t p, double* __restrict__ out_sq,
                            double* __restrict__ out, double* __restrict__ out_inv) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x) {
         const double s = a[j] + add;

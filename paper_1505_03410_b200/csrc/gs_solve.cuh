@@ -23,8 +23,8 @@
 
 namespace gs {
 
-__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+static __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+static __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 struct alignas(16) ColInfo {        // per column, rebuilt per lambda (u), beta kept current
     double ns, inv, nr, u, beta, pad;
@@ -48,7 +48,7 @@ struct SolveCtl {
     int64_t n_screen;
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
+static __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
@@ -116,7 +116,7 @@ struct Group {
     GroupBar* bar;
 };
 
-__device__ __forceinline__ void group_sync(const Group& g) {
+static __device__ __forceinline__ void group_sync(const Group& g) {
     __syncthreads();
     if (g.G > 1) {
         if (threadIdx.x == 0) {
@@ -129,9 +129,13 @@ __device__ __forceinline__ void group_sync(const Group& g) {
                 __threadfence();
                 atomicAdd(&g.bar->gen, 1u);
             } else {
+                // exponential backoff: CTAs idle through a CD epoch must not
+                // flood L2 with polls while CTA 0 runs the latency-bound chain
                 const unsigned long long t0 = gtimer();
+                unsigned ns = 32;
                 while (*genp == my) {
-                    __nanosleep(32);
+                    __nanosleep(ns);
+                    ns = ns < 1024 ? ns * 2 : ns;
                     if (gtimer() - t0 > 60000000000ull) __trap();   // never hang the GPU
                 }
             }
@@ -141,8 +145,53 @@ __device__ __forceinline__ void group_sync(const Group& g) {
     }
 }
 
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
+static __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// bounded spin: a protocol error traps (launch failure) instead of hanging the
+// GPU; the message names the wait and the queue state
+static __device__ __noinline__ void spin_fail(int where, int a, int b, int c, int d) {
+    printf("gapsafe_b200 watchdog: wait %d expired (block %d thread %d: %d %d %d %d)\n", where, (int)blockIdx.x,
+           (int)threadIdx.x, a, b, c, d);
+    __trap();
+}
+static __device__ __forceinline__ void spin_guard(unsigned long long t0, int where = 0, int a = 0, int b = 0, int c = 0,
+                                           int d = 0) {
+    if (gtimer() - t0 > 20000000000ull) spin_fail(where, a, b, c, d);
+}
+
+static __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+static __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+static __device__ __forceinline__ void mbar_expect_tx_s(unsigned b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void mbar_arrive_s(unsigned b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+static __device__ __forceinline__ bool mbar_test_s(unsigned b, unsigned parity) {
+    unsigned ok;
+    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(b), "r"(parity) : "memory");
+    return ok != 0;
+}
+static __device__ __forceinline__ void tma_bulk_g2s_s(unsigned dst, const void* src, unsigned bytes, unsigned b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+static __device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
+// CTA-scope acquire load / release store on shared memory (the load is a
+// plain LDS on sm_100a; the store is MEMBAR.ALL.CTA + STS)
+static __device__ __forceinline__ int ld_acq(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+static __device__ __forceinline__ void st_rel(int* p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -151,7 +200,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // independent predicates are compacted in the same two phases.
 // ---------------------------------------------------------------------------
 template <class PredA, class EmitA, class PredB, class EmitB>
-__device__ void group_compact2(const Group& g, const SolveDev& P, int64_t m, PredA pa, EmitA ea, PredB pb,
+static __device__ void group_compact2(const Group& g, const SolveDev& P, int64_t m, PredA pa, EmitA ea, PredB pb,
                                EmitB eb, int64_t* total_a, int64_t* total_b, int* sh) {
     const int64_t per = (m + g.G - 1) / g.G;
     const int64_t lo = min(m, (int64_t)g.c * per), hi = min(m, lo + per);
@@ -196,10 +245,13 @@ __device__ void group_compact2(const Group& g, const SolveDev& P, int64_t m, Pre
 // ---------------------------------------------------------------------------
 enum GMode : int { G_DUAL = 0, G_CERT = 1, G_MU = 2 };
 
+constexpr int kGStages = 4;     // TMA stages of the staged dense GEMV
+
 template <typename T>
-__device__ void group_gemv(const Group& g, const SolveDev& P, const double* v, const int32_t* cols, int64_t m,
+static __device__ void group_gemv(const Group& g, const SolveDev& P, const double* v, const int32_t* cols, int64_t m,
                            int mode, double* out_c, float* out_t, double rho0, double gam, double radius,
-                           double* vs) {
+                           double* vs, unsigned char* stg = nullptr, int64_t stg_bytes = 0,
+                           int* tile_valid = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = P.n;
     const bool stage = n <= P.vs_cap;
@@ -236,6 +288,87 @@ __device__ void group_gemv(const Group& g, const SolveDev& P, const double* v, c
             const double cval = warp_sum(acc);
             if (lane == 0) epilogue(i, j, cval, nrm, bj);
         }
+    } else if (stg_bytes >= (int64_t)kGStages * P.ld * (int64_t)sizeof(T)) {
+        // TMA-staged: this CTA streams its contiguous share of positions
+        // through kGStages shared-memory stages (cp.async.bulk, mbarrier
+        // tx-count); its warps reduce the columns out of shared memory.  Per
+        // column the lane partition and butterfly are those of ColDot2, so the
+        // values are bit-identical to the direct path below.
+        __shared__ unsigned long long s_gbar[kGStages];
+        const T* X = (const T*)P.X;
+        const int64_t colb = P.ld * (int64_t)sizeof(T);
+        const int64_t sb = stg_bytes / kGStages / 16 * 16;
+        const int C = (int)min((int64_t)(32 * W), sb / colb);      // columns per stage
+        const int64_t per = (m + g.G - 1) / g.G;
+        const int64_t lo = min(m, (int64_t)g.c * per), hi = min(m, lo + per);
+        const int nst = (int)((hi - lo + C - 1) / C);
+        const unsigned bar0 = smem_u32(&s_gbar[0]);
+        const unsigned stg0 = smem_u32(stg);
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < kGStages; ++s) mbar_init(&s_gbar[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        auto issue = [&](int k) {           // warp 0: stage k into slot k % kGStages
+            const int s = k % kGStages;
+            const int64_t i0 = lo + (int64_t)k * C, i1 = min(hi, i0 + C);
+            const unsigned b = bar0 + 8u * s, dst = stg0 + (unsigned)(s * sb);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (lane == 0) mbar_expect_tx_s(b, (unsigned)((i1 - i0) * colb));
+            __syncwarp();
+            if (!cols) {
+                if (lane == 0) tma_bulk_g2s_s(dst, X + i0 * P.ld, (unsigned)((i1 - i0) * colb), b);
+            } else {
+                // one column per lane: the gathered indices load in parallel
+                for (int64_t i = i0 + lane; i < i1; i += 32)
+                    tma_bulk_g2s_s(dst + (unsigned)((i - i0) * colb), X + (int64_t)cols[i] * P.ld, (unsigned)colb, b);
+            }
+        };
+        if (w == 0)
+            for (int k = 0; k < min(nst, kGStages); ++k) issue(k);
+        // per-column epilogue inputs, one stage ahead in registers: lane l of
+        // warp w holds column w + l*W of the stage
+        const int per_w = (C + W - 1) / W;
+        auto fetch = [&](int k, int64_t& jj, double& nr, double& bb) {
+            const int64_t i = lo + (int64_t)k * C + w + (int64_t)lane * W;
+            jj = 0; nr = 0.0; bb = 0.0;
+            if (k < nst && lane < per_w && i < min(hi, lo + (int64_t)(k + 1) * C)) {
+                jj = cols ? (int64_t)cols[i] : i;
+                nr = __ldg(P.norms + jj);
+                if (mode == G_CERT) bb = P.beta[jj];
+            }
+        };
+        int64_t jn; double nn, bn;
+        fetch(0, jn, nn, bn);
+        for (int k = 0; k < nst; ++k) {
+            const int64_t jc = jn; const double nc = nn, bc = bn;
+            fetch(k + 1, jn, nn, bn);
+            const int s = k % kGStages;
+            {
+                const unsigned b = bar0 + 8u * s, par = (unsigned)((k / kGStages) & 1);
+                if (!mbar_test_s(b, par)) {
+                    const unsigned long long t0 = gtimer();
+                    while (!mbar_test_s(b, par)) spin_guard(t0, 5, k, nst, (int)g.c, 0);
+                }
+            }
+            const int64_t i0 = lo + (int64_t)k * C;
+            const int cn = (int)min((int64_t)C, hi - i0);
+            const T* base = reinterpret_cast<const T*>(stg + (size_t)s * sb);
+            for (int l = 0; w + l * W < cn; ++l) {
+                const int cc = w + l * W;
+                const double cval = ColDotS<T>::run(base + (int64_t)cc * P.ld, vv, n, lane);
+                const int64_t j = __shfl_sync(0xffffffffu, jc, l);
+                const double nrm = __shfl_sync(0xffffffffu, nc, l);
+                const double bj = __shfl_sync(0xffffffffu, bc, l);
+                if (lane == 0) epilogue(i0 + cc, j, cval, nrm, bj);
+            }
+            __syncthreads();                  // slot s fully read
+            if (w == 0 && k + kGStages < nst) issue(k + kGStages);
+        }
+        if (threadIdx.x == 0)
+            for (int s = 0; s < kGStages; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&s_gbar[s])) : "memory");
+        if (tile_valid && threadIdx.x == 0) *tile_valid = 0;   // the CD threshold tile was overwritten
+        __syncthreads();
     } else {
         const T* X = (const T*)P.X;
         // each warp takes two columns (i, i + GW) per round
@@ -270,7 +403,7 @@ __device__ void group_gemv(const Group& g, const SolveDev& P, const double* v, c
 }
 
 // max over the per-CTA partials (every caller thread gets the same answer)
-__device__ __forceinline__ void group_max_result(const Group& g, const SolveDev& P, double& v, int64_t& i) {
+static __device__ __forceinline__ void group_max_result(const Group& g, const SolveDev& P, double& v, int64_t& i) {
     v = -1.0;
     i = INT64_MAX;
     for (int k = 0; k < g.G; ++k) argmax_merge(v, i, P.cta_val[k], P.cta_idx[k]);
@@ -281,7 +414,7 @@ __device__ __forceinline__ void group_max_result(const Group& g, const SolveDev&
 // residual resync rho = y - X beta over the support (design_matrix.py:130-137)
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ void group_resync(const Group& g, const SolveDev& P, int64_t m, int* sh) {
+static __device__ void group_resync(const Group& g, const SolveDev& P, int64_t m, int* sh) {
     const int n = P.n;
     // support list S = {A_i : beta_{A_i} != 0}, ascending (l1 norms, dense products)
     const int32_t* A = P.A;
@@ -336,7 +469,7 @@ __device__ void group_resync(const Group& g, const SolveDev& P, int64_t m, int* 
 // checkpoint scalar algebra on CTA 0 (problem.py:98-123, 57-86; regions.py:213-218)
 // l1 over the support list (beta is zero elsewhere).
 // ---------------------------------------------------------------------------
-__device__ void cta_dual(const SolveDev& P, double corr, int want_radius, bool l1_over_support, int64_t m,
+static __device__ void cta_dual(const SolveDev& P, double corr, int want_radius, bool l1_over_support, int64_t m,
                          double* red) {
     DevScalars* sc = P.sc;
     const double lam = P.lam;
@@ -398,7 +531,7 @@ __device__ void cta_dual(const SolveDev& P, double corr, int want_radius, bool l
 
 // post-drop certificate (solver.py:217-221): zero the dropped beta, add the
 // drop-axpy drift to Delta, recompute P with the same theta, trace row.
-__device__ void cta_post(const SolveDev& P, double* red) {
+static __device__ void cta_post(const SolveDev& P, double* red) {
     DevScalars* sc = P.sc;
     SolveCtl* ctl = P.ctl;
     const double lam = P.lam;
@@ -448,7 +581,7 @@ __device__ void cta_post(const SolveDev& P, double* red) {
 // ---------------------------------------------------------------------------
 constexpr int kTTile = 8192;   // certification thresholds staged per tile (float)
 
-__device__ __forceinline__ int64_t scan_tile(const float* ts, int64_t tb, int64_t tend, int64_t from, double D,
+static __device__ __forceinline__ int64_t scan_tile(const float* ts, int64_t tb, int64_t tend, int64_t from, double D,
                                              int lane) {
     for (int64_t base = from; base < tend; base += 32) {
         const int64_t q = base + lane;
@@ -459,7 +592,7 @@ __device__ __forceinline__ int64_t scan_tile(const float* ts, int64_t tb, int64_
     return tend;
 }
 
-__device__ __forceinline__ double delta_step(double D, double step, double rho0) {
+static __device__ __forceinline__ double delta_step(double D, double step, double rho0) {
     // ||rho_new - rho|| <= |d| ||x|| (1+u) + u ||rho_new||, ||rho_new|| <= rho0 + D + |d| ||x||
     return __dadd_ru(D, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12), __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, D), step))));
 }
@@ -506,53 +639,8 @@ struct alignas(16) CdCtl {
     int finished, pad0, pad1, pad2;       // compute warps consumed the current-generation end entry
 };
 
-// bounded spin: a protocol error traps (launch failure) instead of hanging the
-// GPU; the message names the wait and the queue state
-__device__ __noinline__ void spin_fail(int where, int a, int b, int c, int d) {
-    printf("gapsafe_b200 watchdog: wait %d expired (block %d thread %d: %d %d %d %d)\n", where, (int)blockIdx.x,
-           (int)threadIdx.x, a, b, c, d);
-    __trap();
-}
-__device__ __forceinline__ void spin_guard(unsigned long long t0, int where = 0, int a = 0, int b = 0, int c = 0,
-                                           int d = 0) {
-    if (gtimer() - t0 > 20000000000ull) spin_fail(where, a, b, c, d);
-}
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_s(unsigned b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_s(unsigned b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
-}
-__device__ __forceinline__ bool mbar_test_s(unsigned b, unsigned parity) {
-    unsigned ok;
-    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(b), "r"(parity) : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void tma_bulk_g2s_s(unsigned dst, const void* src, unsigned bytes, unsigned b) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(dst), "l"(src), "r"(bytes), "r"(b) : "memory");
-}
-__device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
-// CTA-scope acquire load / release store on shared memory (the load is a
-// plain LDS on sm_100a; the store is MEMBAR.ALL.CTA + STS)
-__device__ __forceinline__ int ld_acq(const int* p) {
-    int v;
-    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_rel(int* p, int v) {
-    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-
 // first position in [from, lim) with !(D < t) (uncertified under D)
-__device__ __forceinline__ int scan_under(const float* ts, int tb, int lim, int from, double D, int lane) {
+static __device__ __forceinline__ int scan_under(const float* ts, int tb, int lim, int from, double D, int lane) {
     for (int base = from; base < lim; base += 32) {
         const int q = base + lane;
         const bool unc = q < lim && !(D < (double)ts[q - tb]);
@@ -578,7 +666,7 @@ __host__ __device__ inline size_t cd_smem_bytes_rt(int64_t ld, int es) {
 }
 
 template <typename T, int R>
-__device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int W, unsigned char* smem,
+static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int W, unsigned char* smem,
                                             int* tile_valid) {
     SolveCtl* ctl = P.ctl;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -893,7 +981,7 @@ __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m64, int 
 }
 
 // CSC: one warp, rho in shared memory after the threshold tile.
-__device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m, unsigned char* smem) {
+static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m, unsigned char* smem) {
     SolveCtl* ctl = P.ctl;
     const int tid = threadIdx.x, lane = tid & 31;
     float* ts = reinterpret_cast<float*>(smem);
@@ -976,7 +1064,7 @@ __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m, unsigned
 // the persistent solve kernel
 // ---------------------------------------------------------------------------
 template <typename T, int R>
-__device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* smem) {
+static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* smem) {
     __shared__ int sh[32];
     __shared__ double red[32];
     DevScalars* sc = P.sc;
@@ -1023,7 +1111,7 @@ __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* sme
             group_sync(g);
             if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
             const unsigned long long ts0 = gtimer();
-            group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, gam, sc->radius, vs);
+            group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, gam, sc->radius, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
             group_sync(g);
             if (g.c == 0 && threadIdx.x == 0) { ctl->t_screen += gtimer() - ts0; ctl->n_screen++; }
         } else if (P.init_mode == 0) {
@@ -1091,7 +1179,7 @@ __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* sme
             group_resync<T>(g, P, m, sh);
             if (m == 0) {
                 // everything screened: unrestricted dual point (solver.py:190-203)
-                group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs);
+                group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
                 group_sync(g);
                 if (g.c == 0) {
                     double corr; int64_t ci;
@@ -1113,7 +1201,7 @@ __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* sme
                 if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
             } else {
                 // restricted |X_A^T rho|_inf with the dots kept for mu and the anchor
-                group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, P.c, nullptr, 0.0, gam, 0.0, vs);
+                group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, P.c, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
                 group_sync(g);
                 if (g.c == 0) {
                     double corr; int64_t ci;
@@ -1238,7 +1326,7 @@ __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* sme
         if (P.certify && ctl->need_refresh && m > 0) {
             const unsigned long long tr0 = gtimer();
             const double anchor = sc->rho_norm_ub;
-            group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0, vs);
+            group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
             if (g.c == 0 && threadIdx.x == 0) { ctl->anchor_norm = anchor; ctl->cd_delta = 0.0; ctl->n_refresh++; s_tile_valid = 0; }
             group_sync(g);
             if (g.c == 0 && threadIdx.x == 0) ctl->t_refresh += gtimer() - tr0;
@@ -1260,8 +1348,8 @@ __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* sme
     if (!converged) {
         const int64_t m = sc->m;
         group_resync<T>(g, P, m, sh);
-        if (m > 0) group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs);
-        else group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs);
+        if (m > 0) group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
+        else group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
         group_sync(g);
         if (g.c == 0) {
             double corr; int64_t ci;
@@ -1311,7 +1399,8 @@ __global__ void __launch_bounds__(256, 1) k_cd_pass_prod(const SolveDev* __restr
     const double anchor = __dsqrt_ru(block_sum_ru(a, red));
     const double gam = gamma_n(P.n);
     if (P.certify) group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0,
-                                 reinterpret_cast<double*>(smem + (P.sparse ? 0 : P.cd_bytes)));
+                                 reinterpret_cast<double*>(smem + (P.sparse ? 0 : P.cd_bytes)), smem,
+                                 P.sparse ? 0 : P.cd_bytes, nullptr);
     if (threadIdx.x == 0) { P.ctl->anchor_norm = anchor; P.ctl->cd_delta = 0.0; }
     __syncthreads();
     __shared__ int s_tile_valid;
@@ -1329,7 +1418,8 @@ __global__ void __launch_bounds__(256, 1) k_screen_full(const SolveDev* __restri
     const SolveDev& P = probs[0];
     Group g{(int)gridDim.x, (int)blockIdx.x, nullptr};
     group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, 0.0, radius,
-                  reinterpret_cast<double*>(smem));
+                  reinterpret_cast<double*>(smem + (P.sparse ? 0 : P.cd_bytes)), smem, P.sparse ? 0 : P.cd_bytes,
+                  nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -1380,7 +1470,8 @@ __global__ void __launch_bounds__(256, 1) k_batch_path(SolveDev* probs, const Ba
             __syncthreads();
             if (gap_rule) {
                 group_gemv<T>(g, sp, sp.theta, nullptr, p, G_MU, nullptr, nullptr, 0.0, 0.0, 0.0,
-                              reinterpret_cast<double*>(smem + (sp.sparse ? 0 : sp.cd_bytes)));
+                              reinterpret_cast<double*>(smem + (sp.sparse ? 0 : sp.cd_bytes)), smem,
+                              sp.sparse ? 0 : sp.cd_bytes, nullptr);
             } else {
                 for (int64_t j = threadIdx.x; j < p; j += blockDim.x) sp.mark[j] = __ldg(sp.norms + j) > 0.0;
             }

@@ -5,23 +5,29 @@ import numpy as np
 import paper_1505_03410_b200 as gs
 from paper_1505_03410_b200 import synth
 
-name = sys.argv[1] if len(sys.argv) > 1 else "cfg0"
-kw = {}
-if len(sys.argv) > 2:
-    kw["p"] = int(sys.argv[2])
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("name", nargs="?", default="cfg0")
+ap.add_argument("p", nargs="?", type=int, default=None)
+ap.add_argument("--once", action="store_true", help="time the first (cold) path only")
+ap.add_argument("--lambdas", type=int, default=None, help="first T lambdas only")
+a = ap.parse_args()
+name = a.name
+kw = {} if a.p is None else {"p": a.p}
 c = synth.by_name(name, **kw)
 t0 = time.perf_counter()
 X = gs.DesignMatrix(c.X)
 dev = gs.DeviceSolver(X, c.y)
-grid = gs.lambda_grid(dev.lambda_max, c.n_lambdas, c.delta)
+grid = gs.lambda_grid(dev.lambda_max, c.n_lambdas, c.delta)[: a.lambdas]
 cfg = gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000)
 t1 = time.perf_counter()
 res = gs.run_path(X, c.y, grid, cfg, solver=dev)
 t2 = time.perf_counter()
-res = gs.run_path(X, c.y, grid, cfg, solver=dev)
+if not a.once:
+    res = gs.run_path(X, c.y, grid, cfg, solver=dev)
 t3 = time.perf_counter()
 st = [s.stats for s in res.states]
-out = dict(config=name, upload_s=t1 - t0, path_s_first=t2 - t1, path_s=t3 - t2,
+out = dict(config=name, upload_s=t1 - t0, path_s_first=t2 - t1, path_s=(t3 - t2) if not a.once else (t2 - t1), lambdas=int(grid.size), n=int(c.X.shape[0]), p=int(c.X.shape[1]),
            epochs=int(sum(s.passes_done for s in res.states)),
            checkpoints=int(sum(x["checkpoints"] for x in st)),
            cd_visits=int(sum(x["cd_visits"] for x in st)),
