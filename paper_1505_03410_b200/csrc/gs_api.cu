@@ -520,13 +520,13 @@ static size_t cd_bytes_for(const gs_matrix* M) {
 static size_t solve_smem(const gs_matrix* M) {
     const int64_t n = M->n;
     const size_t vs = (n <= vs_cap_for(M)) ? (size_t)(n + 2) * 8 : 0;
-    if (M->sparse) return std::max(vs, (size_t)kTTile * sizeof(float) + (size_t)n * 8);
+    if (M->sparse) return std::max(vs, cd_csc_smem_bytes(n));
     return cd_bytes_for(M) + vs;     // dense: CD tile + column ring stay resident beside the GEMV staging
 }
 
 static int check_shape(const gs_matrix* M) {
     if (M->sparse) {
-        if (solve_smem(M) > 220 * 1024) return fail(GS_ERR_VALUE, "sparse solver supports n <= 24576 in this build");
+        if (solve_smem(M) > 225 * 1024) return fail(GS_ERR_VALUE, "sparse solver supports n <= 22400 in this build");
         return GS_OK;
     }
     if (cd_shape(M->n).R == 0) return fail(GS_ERR_VALUE, "dense solver supports n <= 1792 in this build");

@@ -980,76 +980,290 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     __syncthreads();
 }
 
-// CSC: one warp, rho in shared memory after the threshold tile.
-static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m, unsigned char* smem) {
+// CSC CD epoch: conflict-free waves (rho in shared memory).
+//
+// Coordinates whose columns share no row commute exactly: each reads and
+// writes only the rho entries of its own rows.  Warp 0 schedules a wave over
+// the positions [a, b): it walks them in order, skips those certified under a
+// pessimistic drift bound dp = Delta + margin, and admits uncertified ones
+// ("members") while their row sets are pairwise disjoint (a shared-memory row
+// bitmap); the wave ends at the first conflicting candidate, a column with more
+// than 32 nonzeros (run alone), 32 members or the tile end.  All warps then
+// run the members' updates in parallel -- each reads exactly the rho values the
+// sequential order would give it, so the arithmetic is the sequential CD's,
+// bit for bit.  Afterwards the real drift of every skipped position is known
+// (Delta + the members' steps before it); if one of them is no longer
+// certified, the members after it are rolled back exactly (disjoint rows: the
+// old rho values are restored) and the next wave starts at that position.
+constexpr int kSpTile = 4096;    // thresholds + positions staged per tile
+constexpr int kSpMW = 32;        // members per wave (one per lane of warp 0)
+
+struct SpMember {
+    int32_t pos, j, nnz, pad;
+    double ns, nr, bj, d, nb, step;
+    int32_t idx[32];
+    double val[32];
+};
+
+__host__ __device__ inline size_t cd_csc_smem_bytes(int64_t n) {
+    const size_t a = (size_t)kSpTile * 8 + (size_t)n * 8 + (size_t)((n + 31) / 32) * 4;
+    return (a + 15) / 16 * 16 + (size_t)kSpMW * sizeof(SpMember);
+}
+
+static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m64, unsigned char* smem) {
     SolveCtl* ctl = P.ctl;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
+    const int n = P.n, m = (int)m64;
+    const unsigned FULL = 0xffffffffu;
     float* ts = reinterpret_cast<float*>(smem);
-    double* srho = reinterpret_cast<double*>(smem + kTTile * sizeof(float));
-    const int n = P.n;
+    int32_t* As = reinterpret_cast<int32_t*>(smem + kSpTile * 4);
+    double* srho = reinterpret_cast<double*>(smem + kSpTile * 8);
+    const int nbw = (n + 31) / 32;
+    unsigned* bm = reinterpret_cast<unsigned*>(srho + n);
+    SpMember* mem = reinterpret_cast<SpMember*>(smem + ((size_t)kSpTile * 8 + (size_t)n * 8 + (size_t)nbw * 4 + 15) / 16 * 16);
+    __shared__ double s_D;
+    __shared__ int s_a, s_b, s_nmem, s_solo, s_tb, s_tend;
+    const bool use_t = P.certify != 0;
+    const double lam = P.lam;
+    const double rho0 = ctl->anchor_norm;
     for (int r = tid; r < n; r += blockDim.x) srho[r] = P.rho[r];
+    for (int k = tid; k < nbw; k += blockDim.x) bm[k] = 0u;
+    if (tid == 0) { s_D = use_t ? ctl->cd_delta : 0.0; s_a = 0; s_tb = 0; s_tend = 0; }
+    double gstep = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * lam;     // warp 0's copy
+    long long n_unc = 0, n_nz = 0, n_roll = 0, n_mem = 0;                 // warp 0 lane 0
     __syncthreads();
-    if (tid < 32 && m > 0) {
-        const bool use_t = P.certify != 0;
-        double D = use_t ? ctl->cd_delta : 0.0;
-        const double rho0 = ctl->anchor_norm;
-        const double lam = P.lam;
-        int64_t tb = 0, tend = 0, n_unc = 0, n_nz = 0;
-        auto load_tile = [&](int64_t from) {
-            tb = from;
-            tend = min(m, from + (int64_t)kTTile);
-            if (use_t) {
-                for (int64_t q = tb + lane; q < tend; q += 32) ts[q - tb] = P.t[q];
-                __syncwarp();
+    while (s_a < m) {
+        const int a = s_a;
+        if (a >= s_tend) {                       // stage the next tile of thresholds / positions
+            const int tb = a, tend = min(m, a + kSpTile);
+            for (int q = tb + tid; q < tend; q += blockDim.x) {
+                As[q - tb] = P.A[q];
+                ts[q - tb] = use_t ? P.t[q] : -1.0f;
             }
-        };
-        auto scan = [&](int64_t from) -> int64_t {
-            if (!use_t) return from < tend ? from : tend;
-            return scan_tile(ts, tb, tend, from, D, lane);
-        };
-        load_tile(0);
-        int64_t i = scan(0);
-        while (true) {
-            while (i == tend && tend < m) { load_tile(tend); i = scan(tb); }
-            if (i >= m) break;
-            const int32_t j = P.A[i];
-            const double bj = P.beta[j];
-            const double ns = __ldg(P.nsq + j);
-            const int64_t lo = __ldg(P.indptr + j), hi = __ldg(P.indptr + j + 1);
-            double acc = 0.0;
-            for (int64_t q = lo + lane; q < hi; q += 32) acc = fma(__ldg(P.data + q), srho[__ldg(P.indices + q)], acc);
-            const double g = warp_sum(acc);
+            __syncthreads();
+            if (tid == 0) { s_tb = tb; s_tend = tend; }
+            __syncthreads();
+        }
+        const int tb = s_tb, tend = s_tend;
+        // ---------------- schedule (warp 0) ----------------
+        if (w == 0) {
+            const double D = s_D;
+            const double dp = use_t ? __dadd_ru(D, __dmul_ru(2.0 * kSpMW, gstep)) : 0.0;
+            int nmem = 0, b = -1, solo = 0;
+            for (int base = a; b < 0; base += 32) {
+                if (base >= tend) { b = tend; break; }
+                const int q = base + lane;
+                const bool unc = q < tend && (!use_t || !(dp < (double)ts[q - tb]));
+                unsigned mask = __ballot_sync(FULL, unc);
+                if (!mask) continue;
+                // per-candidate column metadata, loaded in parallel by the candidate lanes
+                int cj = 0, cnz = 0;
+                int64_t clo = 0;
+                double cns = 0.0, cnr = 0.0, cbj = 0.0;
+                if (unc) {
+                    cj = As[q - tb];
+                    clo = __ldg(P.indptr + cj);
+                    cnz = (int)(__ldg(P.indptr + cj + 1) - clo);
+                    cns = __ldg(P.nsq + cj);
+                    cnr = __ldg(P.norms + cj);
+                    cbj = P.beta[cj];
+                }
+                while (mask && b < 0) {
+                    // up to 8 candidates: their row lists are loaded together
+                    int cl[8];
+                    unsigned mm = mask;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) { cl[c] = mm ? __ffs(mm) - 1 : -1; if (mm) mm &= mm - 1; }
+                    int ridx[8];
+                    double rval[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        ridx[c] = -1; rval[c] = 0.0;
+                        const int src = cl[c] < 0 ? 0 : cl[c];
+                        const int64_t lo_c = __shfl_sync(FULL, clo, src);
+                        const int nz_c = __shfl_sync(FULL, cnz, src);
+                        if (cl[c] >= 0 && nz_c <= 32 && lane < nz_c) {
+                            ridx[c] = __ldg(P.indices + lo_c + lane);
+                            rval[c] = __ldg(P.data + lo_c + lane);
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        if (cl[c] < 0 || b >= 0) continue;
+                        const int lc = cl[c];
+                        const int pos = base + lc;
+                        const int nz_c = __shfl_sync(FULL, cnz, lc);
+                        if (nz_c > 32) {                  // long column: alone in its wave
+                            if (nmem > 0) { b = pos; break; }
+                            solo = 1;
+                        } else {
+                            const int r = ridx[c];
+                            const bool hit = r >= 0 && ((bm[r >> 5] >> (r & 31)) & 1u);
+                            if (__ballot_sync(FULL, hit)) { b = pos; break; }
+                            if (r >= 0) atomicOr(&bm[r >> 5], 1u << (r & 31));
+                            if (lane < nz_c) { mem[nmem].idx[lane] = r; mem[nmem].val[lane] = rval[c]; }
+                        }
+                        if (lane == lc) {
+                            SpMember& M = mem[nmem];
+                            M.pos = pos; M.j = cj; M.nnz = cnz; M.ns = cns; M.nr = cnr; M.bj = cbj;
+                        }
+                        __syncwarp();
+                        mask &= ~(1u << lc);
+                        ++nmem;
+                        if (solo || nmem == kSpMW) { b = pos + 1; break; }
+                    }
+                }
+            }
+            if (lane == 0) { s_b = b; s_nmem = nmem; s_solo = solo; }
+        }
+        __syncthreads();
+        const int nmem = s_nmem;
+        // ---------------- members in parallel (all warps) ----------------
+        double oldv[kSpMW / 8 > 0 ? (kSpMW + 7) / 8 : 1];
+#pragma unroll
+        for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
+            oldv[it] = 0.0;
+            const int k = w + it * NW;
+            if (k >= nmem) continue;
+            SpMember& M = mem[k];
+            const double bj = M.bj, ns = M.ns;
+            double g;
+            int r = -1;
+            double x = 0.0, o = 0.0;
+            if (!s_solo) {
+                if (lane < M.nnz) { r = M.idx[lane]; x = M.val[lane]; o = srho[r]; }
+                g = warp_sum(fma(x, o, 0.0));
+            } else {
+                const int64_t lo = __ldg(P.indptr + M.j), hi = __ldg(P.indptr + M.j + 1);
+                double acc = 0.0;
+                for (int64_t q = lo + lane; q < hi; q += 32) acc = fma(__ldg(P.data + q), srho[__ldg(P.indices + q)], acc);
+                g = warp_sum(acc);
+            }
             const double z = bj + g / ns;
             const double u = lam / ns;
             const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
             const double d = nb - bj;
-            ++n_unc;
             if (d != 0.0) {
-                ++n_nz;
-                if (lane == 0) {
-                    P.beta[j] = nb;
-                    if (use_t && bj == 0.0) P.t[i] = -1.0f;
+                if (!s_solo) {
+                    if (r >= 0) srho[r] = __dsub_rn(o, __dmul_rn(d, x));
+                } else {
+                    __syncwarp();
+                    const int64_t lo = __ldg(P.indptr + M.j), hi = __ldg(P.indptr + M.j + 1);
+                    for (int64_t q = lo + lane; q < hi; q += 32) {
+                        const int32_t rr = __ldg(P.indices + q);
+                        srho[rr] = __dsub_rn(srho[rr], __dmul_rn(d, __ldg(P.data + q)));
+                    }
                 }
-                for (int64_t q = lo + lane; q < hi; q += 32) {
-                    const int32_t r = __ldg(P.indices + q);
-                    srho[r] = __dsub_rn(srho[r], __dmul_rn(d, __ldg(P.data + q)));
-                }
-                __syncwarp();
-                if (use_t) D = delta_step(D, __dmul_ru(fabs(d), __ldg(P.norms + j)), rho0);
             }
-            i = scan(i + 1);
+            oldv[it] = o;
+            if (lane == 0) { M.d = d; M.nb = nb; M.step = d != 0.0 ? __dmul_ru(fabs(d), M.nr) : 0.0; }
         }
-        if (lane == 0) {
-            ctl->cd_delta = D;
-            ctl->epoch_unc = n_unc;
-            ctl->epoch_nz = n_nz;
-            P.sc->visits += (unsigned long long)m;
-            P.sc->uncertified += (unsigned long long)n_unc;
-            P.sc->nonzero += (unsigned long long)n_nz;
+        __syncthreads();
+        // ---------------- drift bound, certification check, cut-off (warp 0) ----------------
+        if (w == 0) {
+            int b = s_b;
+            double Dn = 0.0;
+            if (use_t) {
+                const double D = s_D;
+                const double st = lane < nmem ? mem[lane].step : 0.0;
+                double incl = st;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double t = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl = __dadd_ru(incl, t);
+                }
+                const double S = __shfl_sync(FULL, incl, 31);
+                double excl = __shfl_up_sync(FULL, incl, 1);
+                if (lane == 0) excl = 0.0;
+                // per update: |d| ||x|| (1+1e-12) plus a rounding term u ||rho_new||,
+                // ||rho_new|| <= rho0 + Delta + 2 S (see delta_step)
+                const double err = __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, D), __dmul_ru(2.0, S)));
+                auto Dk = [&](int k, double ex) {     // bound before member k (ex = steps of members < k)
+                    return __dadd_ru(__dadd_ru(D, __dmul_ru(ex, 1.0 + 1e-12)), __dmul_ru((double)k, err));
+                };
+                Dn = Dk(nmem, S);
+                const double dp = __dadd_ru(D, __dmul_ru(2.0 * kSpMW, gstep));
+                if (Dn > dp) {
+                    // find the first skipped position whose certificate fails under its real drift
+                    int cut = -1;
+                    for (int base = a; base < b && cut < 0; base += 32) {
+                        const int s = base + lane;
+                        bool bad = false;
+                        if (s < b) {
+                            int k = 0;                         // members before s
+                            bool is_mem = false;
+                            for (int q = 0; q < nmem; ++q) {
+                                const int pq = mem[q].pos;
+                                k += pq < s ? 1 : 0;
+                                is_mem |= pq == s;
+                            }
+                            if (!is_mem) {
+                                double ex = 0.0;               // steps of the members before s
+                                for (int q = 0; q < k; ++q) ex = __dadd_ru(ex, mem[q].step);
+                                bad = !(Dk(k, ex) < (double)ts[s - tb]);
+                            }
+                        }
+                        const unsigned bb = __ballot_sync(FULL, bad);
+                        if (bb) cut = base + __ffs(bb) - 1;
+                    }
+                    if (cut >= 0) {
+                        b = cut;
+                        int k = 0;
+                        double ex = 0.0;
+                        for (int q = 0; q < nmem; ++q)
+                            if (mem[q].pos < cut) { ++k; ex = __dadd_ru(ex, mem[q].step); }
+                        Dn = Dk(k, ex);
+                        if (lane == 0) ++n_roll;
+                    }
+                }
+            }
+            // kept members: statistics and the step estimate
+            if (lane == 0) {
+                for (int q = 0; q < nmem; ++q) {
+                    if (mem[q].pos >= b) break;
+                    ++n_unc;
+                    if (mem[q].d != 0.0) { ++n_nz; gstep = 0.875 * gstep + 0.125 * mem[q].step; }
+                }
+                n_mem += nmem;
+                s_b = b;
+                if (use_t) s_D = Dn;
+            }
+            gstep = __shfl_sync(FULL, gstep, 0);
         }
-    } else if (tid == 0 && m == 0) {
-        ctl->epoch_unc = 0;
-        ctl->epoch_nz = 0;
+        __syncthreads();
+        // ---------------- commit or roll back; release the rows ----------------
+        {
+            const int b = s_b;
+#pragma unroll
+            for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
+                const int k = w + it * NW;
+                if (k >= nmem) continue;
+                const SpMember& M = mem[k];
+                const bool keep = M.pos < b;
+                if (!s_solo && lane < M.nnz) {
+                    const int r = M.idx[lane];
+                    if (!keep && M.d != 0.0) srho[r] = oldv[it];
+                    atomicAnd(&bm[r >> 5], ~(1u << (r & 31)));
+                }
+                if (keep && M.d != 0.0 && lane == 0) {
+                    P.beta[M.j] = M.nb;
+                    if (use_t && M.bj == 0.0) { P.t[M.pos] = -1.0f; ts[M.pos - tb] = -1.0f; }
+                }
+            }
+            if (tid == 0) s_a = b;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ctl->cd_delta = s_D;
+        ctl->cd_gstep = gstep;
+        ctl->epoch_unc = n_unc;
+        ctl->epoch_nz = n_nz;
+        ctl->n_requeue += n_roll;
+        ctl->n_cand += n_mem;
+        P.sc->visits += (unsigned long long)m;
+        P.sc->uncertified += (unsigned long long)n_unc;
+        P.sc->nonzero += (unsigned long long)n_nz;
     }
     __syncthreads();
     __shared__ double red[32];

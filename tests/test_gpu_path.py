@@ -184,3 +184,42 @@ def test_problem_algebra_hand_values():
     np.testing.assert_allclose(t.theta, [0.5, 0.5])
     assert t.feasibility_margin == pytest.approx(0.0, abs=1e-15)
     assert gs.dual_scale(prob, np.zeros(2)).interpolating
+
+
+def _ragged_csc(seed, n, p, max_nnz):
+    """CSC with column lengths 1..max_nnz (some above 32: such columns run
+    alone in their wave), lognormal values, unit norms."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, max_nnz + 1, size=p)
+    rows = [np.sort(rng.choice(n, size=k, replace=False)) for k in lens]
+    vals = [rng.lognormal(size=k) for k in lens]
+    vals = [v / np.linalg.norm(v) for v in vals]
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    X = sp.csc_matrix((np.concatenate(vals), np.concatenate(rows).astype(np.int32), indptr), shape=(n, p))
+    beta = np.zeros(p)
+    beta[rng.choice(p, 40, replace=False)] = rng.choice([-1.0, 1.0], 40)
+    y = X @ beta
+    y += rng.standard_normal(n) * np.linalg.norm(y) / np.sqrt(n) / 4
+    return X, y
+
+
+@pytest.mark.parametrize("n,p,max_nnz", [(400, 3000, 12), (1500, 6000, 60), (5000, 8000, 30)])
+def test_path_sparse_waves_ragged(n, p, max_nnz):
+    """Conflict-free wave CD on ragged CSC columns (row conflicts, long
+    columns, rollbacks) against the oracle path."""
+    X, y = _ragged_csc(n + p, n, p, max_nnz)
+    ra, rb, yy = _paths(X, y, 12, 2.0, 1e-8 * float(y @ y))
+    compare_paths(ra, rb, yy)
+
+
+def test_path_sparse_certify_identical():
+    """Certified skipping and rollback are exact on the CSC path too."""
+    X, y = _ragged_csc(7, 1200, 5000, 40)
+    Xd = gs.DesignMatrix(X)
+    dev = gs.DeviceSolver(Xd, y)
+    grid = gs.lambda_grid(dev.lambda_max, 12, 2.0)
+    eps = 1e-8 * float(y @ y)
+    a = gs.run_path(Xd, y, grid, gs.SolverConfig(epsilon=eps, max_passes=100_000), solver=dev)
+    b = gs.run_path(Xd, y, grid, gs.SolverConfig(epsilon=eps, max_passes=100_000, certify=False), solver=dev)
+    assert np.array_equal(a.betas, b.betas)
+    assert [x.gap for x in a.certs] == [x.gap for x in b.certs]
