@@ -193,6 +193,24 @@ static __device__ __forceinline__ int ld_acq(const int* p) {
 static __device__ __forceinline__ void st_rel(int* p, int v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
+// the same on precomputed 32-bit shared addresses: no generic->shared
+// conversion (S2UR SR_CgaCtaId) inside the serial loops
+static __device__ __forceinline__ int ld_acq_s(unsigned a) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+static __device__ __forceinline__ void st_rel_s(unsigned a, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+static __device__ __forceinline__ void st_vol_f64_s(unsigned a, double v) {
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+static __device__ __forceinline__ double ld_vol_f64_s(unsigned a) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
 
 // ---------------------------------------------------------------------------
 // group-wide stable compaction over positions [0, m): each CTA owns one
@@ -605,12 +623,11 @@ static __device__ __forceinline__ double delta_step(double D, double step, doubl
 //     candidate into its own ring slot: two TMA bulk copies (cp.async.bulk,
 //     mbarrier complete_tx) for the column x_j (ld*sizeof(T) bytes) and its
 //     packed ColInfo (nsq, 1/nsq, ||x||, u = lam/nsq, beta), then the slot
-//     header (position, threshold, Dp, generation).  Headers are published at
-//     once (hdr_ready); data readiness is published in order as the TMA
-//     transactions complete (data_ready).
-//   compute warps (0..W-1): read the next header; skip candidates certified
-//     under the current Delta without waiting for their data; otherwise wait
-//     for data_ready and run the chain  dot -> butterfly [-> cross-warp sum] ->
+//     header (position, threshold, Dp, generation).  Entries are published
+//     in order as their TMA transactions complete (data_ready).
+//   compute warps (0..W-1): one poll per entry; skip candidates certified
+//     under the current Delta, otherwise run the chain
+//     dot -> butterfly [-> cross-warp sum] ->
 //     RN(g/nsq) (RN(1/nsq) + Markstein) -> soft threshold -> axpy, then publish
 //     Delta.  If Delta outgrew an entry's Dp, positions between candidates may
 //     no longer be certified: restart after the last processed position with a
@@ -631,7 +648,6 @@ struct alignas(16) SlotHdr {
 
 struct alignas(16) CdCtl {
     unsigned long long bar[kRingMax];     // mbarriers (TMA completion), one per slot
-    int hdr_ready[kRingMax];              // entry index + 1 whose header is in the slot
     int data_ready[kRingMax];             // entry index + 1 whose bytes have landed
     int consumed[8];                      // per compute warp: entries fully read
     double dpub;                          // Delta published by compute warp 0
@@ -690,7 +706,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     }
     // ---- setup (all threads)
     if (tid == 0) {
-        for (int s = 0; s < K; ++s) { mbar_init(&cc->bar[s], 1); cc->hdr_ready[s] = 0; cc->data_ready[s] = 0; }
+        for (int s = 0; s < K; ++s) { mbar_init(&cc->bar[s], 1); cc->data_ready[s] = 0; }
         for (int k = 0; k < 8; ++k) cc->consumed[k] = 0;
         cc->dpub = use_t ? ctl->cd_delta : 0.0;
         cc->req_gen = 0;
@@ -709,6 +725,11 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     __syncthreads();
     const unsigned ring_s = smem_u32(ring);
     const unsigned bar_s = smem_u32(&cc->bar[0]);
+    // control words as 32-bit shared addresses, computed once
+    const unsigned dat_s = smem_u32(&cc->data_ready[0]);
+    const unsigned cons_s = smem_u32(&cc->consumed[0]), fin_s = smem_u32(&cc->finished);
+    const unsigned reqg_s = smem_u32(&cc->req_gen), reqp_s = smem_u32(&cc->req_pos);
+    const unsigned dpub_s = smem_u32(&cc->dpub);
 
     if (w == W && W < (int)(blockDim.x >> 5)) {
         // =================== producer warp ===================
@@ -730,12 +751,12 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
         // every control word is read by lane 0 and broadcast: the warp must take
         // uniform decisions (ballots and shuffles below use the full mask)
         auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
-        while (!bcast(lane == 0 ? ld_acq(&cc->finished) : 0)) {
+        while (!bcast(lane == 0 ? ld_acq_s(fin_s) : 0)) {
             // restart request from the compute warps
-            const int rg = bcast(lane == 0 ? ld_acq(&cc->req_gen) : 0);
+            const int rg = bcast(lane == 0 ? ld_acq_s(reqg_s) : 0);
             if (rg != gen) {
                 gen = rg;
-                const int rp = bcast(lane == 0 ? ld_acq(&cc->req_pos) : 0);
+                const int rp = bcast(lane == 0 ? ld_acq_s(reqp_s) : 0);
                 if (rp < tb || rp > tend || (rp == tend && tend < m)) load_tile_p(rp);
                 qnext = rp;
                 done = false;
@@ -747,14 +768,14 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 if (lane == 0) ok = mbar_test_s(bar_s + 8u * s, (unsigned)((k_data >> kshift) & 1));
                 ok = __shfl_sync(0xffffffffu, ok, 0);
                 if (!ok) break;
-                if (lane == 0) st_rel(&cc->data_ready[s], k_data + 1);
+                if (lane == 0) st_rel_s(dat_s + 4u * s, k_data + 1);
                 ++k_data;
                 t0 = gtimer();
             }
             // free slots: entries consumed by every compute warp and whose bytes landed
             int cmin = 0x7fffffff;
             if (lane == 0)
-                for (int q = 0; q < W; ++q) cmin = min(cmin, ld_acq(&cc->consumed[q]));
+                for (int q = 0; q < W; ++q) cmin = min(cmin, ld_acq_s(cons_s + 4u * q));
             cmin = bcast(cmin);
             const int free_slots = min(K - (k_issue - cmin), K - (k_issue - k_data));
             if (done || free_slots <= 0) {
@@ -763,7 +784,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 continue;
             }
             // one ballot: every candidate of the next window
-            double dpub = lane == 0 ? *(const volatile double*)&cc->dpub : 0.0;
+            double dpub = lane == 0 ? ld_vol_f64_s(dpub_s) : 0.0;
             dpub = __shfl_sync(0xffffffffu, dpub, 0);
             const double dp = use_t ? __dadd_ru(dpub, margin_gs) : 0.0;
             int base = qnext;
@@ -804,7 +825,6 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                     h->pos = p;
                     h->j = j;
                     h->gen = gen;
-                    st_rel(&cc->hdr_ready[s], k + 1);
                 }
                 // position of the last issued candidate (rank navail-1)
                 int lastbit = 0;
@@ -823,7 +843,6 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                     h->pos = m;
                     h->gen = gen;
                     mbar_arrive_s(bar_s + 8u * s);
-                    st_rel(&cc->hdr_ready[s], k_issue + 1);
                 }
                 ++k_issue;
                 done = true;
@@ -852,23 +871,33 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
         int pb = 0, gen = 0, last = -1;
         int n_unc = 0, n_nz = 0, n_req = 0, n_cand = 0, n_skip = 0;
         const int cmask = min(7, (K >> 2) - 1);     // consumed is signalled every cmask+1 entries
+        const unsigned mycons_s = cons_s + 4u * w;
         for (int k = 0;; ++k) {
             const int s = k & kmask;
-            if (ld_acq(&cc->hdr_ready[s]) != k + 1) {
+            // one poll per entry: header and bytes are published together (in order)
+            if (ld_acq_s(dat_s + 4u * s) != k + 1) {
                 const unsigned long long t0 = gtimer();
-                while (ld_acq(&cc->hdr_ready[s]) != k + 1) spin_guard(t0, 3, k, ld_acq(&cc->hdr_ready[s]), gen, last);
+                while (ld_acq_s(dat_s + 4u * s) != k + 1) spin_guard(t0, 4, k, ld_acq_s(dat_s + 4u * s), gen, last);
             }
             const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
             const int pos = h->pos;
             const int hg = h->gen;
             const double tc = h->tcert, dp = h->dp;
+            const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
+            const int32_t j = h->j;
+            const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
+            double xv[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
+            // consumed is signalled in batches (release store; the slot is fully read)
+            if ((k & cmask) == cmask) { __syncwarp(); if (lane == 0) st_rel_s(mycons_s, k + 1); }
             bool process = hg == gen && pos < m;
             if (process && use_t) {
                 if (D > dp) {
                     // drift outgrew the queue's bound: restart after the last processed position
                     ++n_req;
                     ++gen;
-                    if (tid == 0) { *(volatile int*)&cc->req_pos = last + 1; st_rel(&cc->req_gen, gen); }
+                    if (tid == 0) { st_rel_s(reqp_s, last + 1); st_rel_s(reqg_s, gen); }
                     process = false;
                 } else if (D < tc) {
                     ++n_skip;                              // certified: zero update
@@ -876,27 +905,14 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 }
             }
             if (!process) {
-                // consumed is signalled in batches of 8 entries (release store)
-                if ((k & cmask) == cmask) { __syncwarp(); if (lane == 0) st_rel(&cc->consumed[w], k + 1); }
                 if (hg == gen && pos >= m) {
-                    if (tid == 0) st_rel(&cc->finished, 1);
+                    if (tid == 0) st_rel_s(fin_s, 1);
                     break;
                 }
                 if (hg == gen) ++n_cand;
                 continue;
             }
             ++n_cand;
-            if (ld_acq(&cc->data_ready[s]) != k + 1) {
-                const unsigned long long t0 = gtimer();
-                while (ld_acq(&cc->data_ready[s]) != k + 1) spin_guard(t0, 4, k, ld_acq(&cc->data_ready[s]), gen, last);
-            }
-            const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
-            const int32_t j = h->j;
-            const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
-            double xv[R];
-#pragma unroll
-            for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
-            if ((k & cmask) == cmask) { __syncwarp(); if (lane == 0) st_rel(&cc->consumed[w], k + 1); }   // slots fully read
             // ---- critical chain
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -932,15 +948,15 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                     D = delta_step(D, step, rho0);
                     gstep = 0.875 * gstep + 0.125 * step;
                 }
-                if (tid == 0) {
-                    beta[j] = nb;
-                    cinfo_w[j].beta = nb;
-                    if (use_t && bj == 0.0) {
-                        tg[pos] = -1.0f;                       // now in the support
-                        if (m <= kTTile) ts[pos] = -1.0f;      // resident tile (single tile only)
-                    }
-                    *(volatile double*)&cc->dpub = D;
+                // bookkeeping stores by every lane of every compute warp (same
+                // value, same address): no divergent branch in the chain
+                beta[j] = nb;
+                cinfo_w[j].beta = nb;
+                if (use_t && bj == 0.0) {
+                    tg[pos] = -1.0f;                       // now in the support
+                    if (m <= kTTile) ts[pos] = -1.0f;      // resident tile (single tile only)
                 }
+                st_vol_f64_s(dpub_s, D);
             }
         }
         if (W > 1) named_bar(1, BT);

@@ -5,7 +5,8 @@ import paper_1505_03410_b200 as gs
 from paper_1505_03410_b200 import synth
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg0"
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-c = synth.by_name(name)
+kw = {"p": int(sys.argv[3])} if len(sys.argv) > 3 else {}
+c = synth.by_name(name, **kw)
 X = gs.DesignMatrix(c.X)
 dev = gs.DeviceSolver(X, c.y)
 grid = gs.lambda_grid(dev.lambda_max, c.n_lambdas, c.delta)[:T]
