@@ -494,6 +494,11 @@ static CdShape cd_shape(int64_t n) {
     return {0, 0};
 }
 
+// CD consumer per shape (measured on B200, profiles/r01/cd_modes.md): Gram
+// windows win while the member rows fit 4 per lane (cfg0: 10.8 s vs 12.9 s);
+// at 8 rows per lane (cfg1) one reduction per coordinate is faster.
+static int cd_gram_default(int64_t n) { return cd_shape(n).R <= 4 ? 1 : 0; }
+
 static int launch_solve(const gs_matrix* M, cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem,
                         int R) {
     const bool f64 = M->sparse || M->dtype == GS_DTYPE_F64;
@@ -768,6 +773,10 @@ static void fill_dev(gs_solver* S, SolveDev& d) {
     d.vs_cap = vs_cap_for(M);
     const char* env = getenv("GS_REFRESH_EXCESS");
     d.refresh_excess = env ? atoi(env) : 32;
+    const char* eg = getenv("GS_CD_GRAM");
+    d.cd_gram = eg ? atoi(eg) : cd_gram_default(M->n);
+    const char* ep = getenv("GS_CD_PROF");
+    d.cd_prof = ep ? atoi(ep) : 0;
 }
 
 extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* cfg, const int64_t* active0,
@@ -941,6 +950,10 @@ extern "C" int gs_cd_pass(const gs_matrix* M, double* beta, double* rho, const i
             d.data = M->data; d.indices = M->indices; d.indptr = M->indptr;
             d.norms = dnorm; d.nsq = dns; d.inv_nsq = dinv; d.cinfo = dci; d.beta = db; d.rho = dr; d.c = c; d.t = t; d.A = dA;
             d.sc = sc; d.ctl = ctl; d.lam = lam; d.certify = 1; d.cta_val = cval; d.cta_idx = cidx;
+            {
+                const char* eg = getenv("GS_CD_GRAM");
+                d.cd_gram = eg ? atoi(eg) : cd_gram_default(n);
+            }
             d.cd_warps = M->sparse ? 1 : cd_shape(n).W;
             d.cd_bytes = (int)cd_bytes_for(M);
             d.vs_cap = vs_cap_for(M);
@@ -1269,6 +1282,8 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
         d.vs_cap = vs_cap_for(&Bt->shape);
         const char* env = getenv("GS_REFRESH_EXCESS");
         d.refresh_excess = env ? atoi(env) : 32;
+        const char* eg = getenv("GS_CD_GRAM");
+        d.cd_gram = eg ? atoi(eg) : cd_gram_default(n);
         BatchOut& o = outs[b];
         o.grid = dgrid + b * T; o.lmax = Bt->lmax[b]; o.betas = dbetas ? dbetas + b * T * p : nullptr;
         o.passes = dpasses + b * T; o.gaps = dgaps + b * T; o.converged = dconv + b * T; o.n_active = dnact + b * T;

@@ -69,7 +69,7 @@ template <typename T> __device__ __forceinline__ double to_d(T x) { return (doub
 // gamma_n bound for an n-term dot product in any summation order (with or
 // without FMA): |fl(x.v) - x.v| <= gamma * sum|x_r v_r|.
 __host__ __device__ inline double gamma_n(int64_t n) {
-    double nu = (double)(n + 4) * kU;
+    double nu = (double)(n + 40) * kU;    // +36u: the Gram-window consumer's final summations
     return nu / (1.0 - nu) * 1.0001;
 }
 

@@ -46,6 +46,8 @@ struct SolveCtl {
     // device-side phase timers (%globaltimer, ns), CTA 0 thread 0
     unsigned long long t_screen, t_ckpt, t_refresh, t_cd;
     int64_t n_screen;
+    // Gram-window consumer phase cycles (warp 0, clock64), GS_CD_PROF=1
+    unsigned long long c_form, c_wait, c_red, c_chain, c_upd, n_win, n_mem;
 };
 
 static __device__ __forceinline__ unsigned long long gtimer() {
@@ -109,6 +111,8 @@ struct SolveDev {
     int cd_warps;        // CD warp-group size
     int cd_bytes;        // dense CD shared-memory region (tile + ring), GEMV staging after it
     int vs_cap;          // max n staged in shared memory for the GEMV
+    int cd_gram;         // dense CD: Gram-window consumer (1) or one reduction per coordinate (0)
+    int cd_prof;         // print Gram-window phase cycles at the end of each solve (debug)
 };
 
 struct Group {
@@ -624,7 +628,7 @@ static __device__ __forceinline__ double delta_step(double D, double step, doubl
 //     mbarrier complete_tx) for the column x_j (ld*sizeof(T) bytes) and its
 //     packed ColInfo (nsq, 1/nsq, ||x||, u = lam/nsq, beta), then the slot
 //     header (position, threshold, Dp, generation).  Entries are published
-//     in order as their TMA transactions complete (data_ready).
+//     through the slot mbarriers (consumers test the entry's phase).
 //   compute warps (0..W-1): one poll per entry; skip candidates certified
 //     under the current Delta, otherwise run the chain
 //     dot -> butterfly [-> cross-warp sum] ->
@@ -643,16 +647,37 @@ struct alignas(16) SlotHdr {
     int32_t pos;                     // candidate position; == m: end of epoch
     int32_t j;
     int32_t gen;
-    int32_t pad;
+    int32_t flags;                   // kNoData: header-only entry (no column bytes)
 };
+constexpr int32_t kNoData = 1;
 
 struct alignas(16) CdCtl {
     unsigned long long bar[kRingMax];     // mbarriers (TMA completion), one per slot
-    int data_ready[kRingMax];             // entry index + 1 whose bytes have landed
     int consumed[8];                      // per compute warp: entries fully read
     double dpub;                          // Delta published by compute warp 0
     int req_gen, req_pos;                 // restart request (compute -> producer)
     int finished, pad0, pad1, pad2;       // compute warps consumed the current-generation end entry
+    double req_hint;                      // Gram windows: the restarted generation selects under >= this drift
+};
+
+// Gram-window consumer state (shared memory, see cd_consume_gram)
+constexpr int kGM = 7;                                // members per window
+constexpr int kGDots = kGM + kGM * (kGM - 1) / 2;     // h_b and Gram G(b,b'), b' < b: 28 <= 32 lanes
+constexpr int kGEv = 512;                             // window span in positions = P-event capacity
+struct alignas(16) GMem {
+    double tc, dp, bj, ns, iv, uq, nr, pad;
+    int32_t j, pos, pad0, pad1;
+};
+struct alignas(16) GWin {
+    double part[8][32];          // per-warp reduced dots
+    double vals[32];             // window dots: h_b at [b], G(b,b') at [kGM + b(b-1)/2 + b']
+    GMem mem[kGM];
+    double ev_t[kGEv], ev_dp[kGEv];
+    int32_t ev_pos[kGEv], ev_gap[kGEv];
+    unsigned gmin_t[kGM + 1], gmin_dp[kGM + 1];   // per gap: min t, min dp (float bits, dp rounded down)
+    double dres[kGM], nbv[kGM];  // committed updates d_b (0: none) and new coefficients
+    double D, gstep, term_dp;
+    int ncommit, gen, wstart, done;
 };
 
 // first position in [from, lim) with !(D < t) (uncertified under D)
@@ -666,6 +691,363 @@ static __device__ __forceinline__ int scan_under(const float* ts, int tb, int li
     return lim;
 }
 
+// Gram-window consumer (P.cd_gram): the compute warps take the ring entries in
+// windows of up to kGM "members" (candidates uncertified at the window start
+// with a growth allowance: t <= Dq = D_s + Mg, Mg = 2 kGM gstep), load the
+// members' rows into registers, and reduce ALL dots of the window at once --
+// h_b = x_b^T rho and G(b,b') = x_b^T x_b' (b' < b) -- in one transposed
+// butterfly (28 values, lane l ends with dot l).  Warp 0 then runs the
+// coordinate chain in registers, every lane redundantly:
+//     g_b = h_b - sum_{b'<b} d_b' G(b,b')   (accumulated as the d's appear)
+//     z = beta + RN(g/nsq); soft threshold; d_b
+// and the members' axpys rho -= d_b x_b are applied afterwards in member order
+// with the reference's separate roundings (_kernels.py:60-64), so the stored
+// rho is exactly the one sequential CD would store with these d's.
+//
+// The other candidates in the window span ("P events": certified at the
+// window start) are re-checked at their turn against the running drift D: a
+// P position that lost its certificate truncates the window there (members
+// before it commit; the producer restarts at it), and an entry whose producer
+// bound dp no longer covers D (positions between candidates may be
+// uncertified) discards the window (nothing committed; restart at the window
+// start under a larger drift hint).  Window boundaries are a function of the
+// data (thresholds, D), never of timing, so results are bit-identical run to
+// run (pkg/tests/test_path.py:124-131).
+//
+// Safety of skipping with the Gram form of g: relative to x_b^T rho_stored
+// it adds the dot errors of h and G (<= gam ||x_b|| (||rho0|| + 2 Delta)),
+// the missed axpy roundings x_b^T e_b' (<= ||x_b|| * the rounding part of
+// each step, hence the doubled allowance in delta_step_g) and the final
+// summation (<= 8u (|h| + sum |d G|)); gamma_n carries +40u for the latter,
+// so cert_threshold's bound still implies a zero update.
+static __device__ __forceinline__ double delta_step_g(double D, double step, double rho0) {
+    return __dadd_ru(D, __dadd_ru(__dmul_ru(step, 1.0 + 1e-12), __dmul_ru(4.6e-16, __dadd_ru(__dadd_ru(rho0, D), step))));
+}
+
+template <typename T, int R>
+static __device__ __forceinline__ void cd_consume_gram(const SolveDev& P, const int m, const int W,
+                                                       const unsigned char* ring, const unsigned sbytes, const int kmask,
+                                                       const unsigned bar_s, const int kshift, const unsigned cons_s, const unsigned fin_s,
+                                                       const unsigned reqg_s, const unsigned reqp_s, const unsigned dpub_s,
+                                                       CdCtl* cc, GWin* gw, float* ts, const bool use_t, const double rho0,
+                                                       double (&rr)[R], double& D, double& gstep, int& n_unc, int& n_nz,
+                                                       int& n_req, int& n_cand, int& n_skip, const int ct) {
+    const int tid = ct, lane = tid & 31, w = tid >> 5, BT = W * 32;
+    const unsigned FULL = 0xffffffffu;
+    const int n = P.n;
+    const unsigned mycons_s = cons_s + 4u * w;
+    const unsigned lower = (1u << lane) - 1u;
+    int k = 0, gen = 0, wstart = 0;
+    double xw[kGM][R];
+#pragma unroll
+    for (int b = 0; b < kGM; ++b)
+#pragma unroll
+        for (int q = 0; q < R; ++q) xw[b][q] = 0.0;
+    for (;;) {
+        const double Mg = use_t ? __dmul_ru((double)kGM, gstep) : 0.0;
+        const double Dq = use_t ? __dadd_ru(D, Mg) : 0.0;
+        const int span_end = wstart + kGEv;
+        int nmem = 0, nev = 0, term = 0, lastpos = -1, termpos = 0, ncand = 0;
+        double term_dp = 0.0;
+        // member b's header fields live in lane b of warp 0
+        double m_tc = 0.0, m_dp = 0.0, m_bj = 0.0, m_ns = 0.0, m_iv = 0.0, m_uq = 0.0, m_nr = 0.0;
+        int m_j = 0, m_pos = 0;
+        const long long c0 = clock64();
+        long long cw = 0;
+        // ---------------- formation (every compute warp, identically) ----------------
+        unsigned long long t0 = 0;
+        while (term == 0) {
+            const int idx = k + lane;
+            const int s = idx & kmask;
+            // entry idx is ready when its slot's phase (idx / K) & 1 completed; only
+            // the next K entries can be tested (one use ahead at most)
+            const bool rdy = lane <= kmask && mbar_test_s(bar_s + 8u * s, (unsigned)((idx >> kshift) & 1));
+            const unsigned rb = __ballot_sync(FULL, rdy);
+            const int nr = (rb == FULL) ? 32 : __ffs(~rb) - 1;
+            if (nr == 0) {
+                const long long cs = clock64();
+                if (t0 == 0) t0 = gtimer();
+                spin_guard(t0, 6, k, gen, wstart, nmem);
+                cw += clock64() - cs;
+                continue;
+            }
+            t0 = 0;
+            const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
+            int hg = -1, pos = 0, fl = 0;
+            double tc = 0.0, dp = 0.0;
+            if (lane < nr) { hg = h->gen; pos = h->pos; fl = h->flags; tc = h->tcert; dp = h->dp; }
+            const bool live = lane < nr && hg == gen;
+            const bool isend = live && pos >= m;
+            const bool beyond = live && !isend && pos >= span_end;
+            const bool inwin = live && !isend && !beyond;
+            const bool isq = inwin && (!use_t || !(Dq < tc));
+            const bool anom = live && use_t && ((dp < Dq) || (isq && (fl & kNoData)));
+            const unsigned qb = __ballot_sync(FULL, isq);
+            const unsigned tb = __ballot_sync(FULL, isend || beyond || anom);
+            const int tpos = tb ? __ffs(tb) - 1 : 32;
+            const int need = kGM - nmem;
+            const int lastq = (__popc(qb) >= need) ? (int)__fns(qb, 0, need) : 32;   // need-th member
+            int cut, tkind = 0;
+            if (lastq < tpos) {
+                cut = lastq + 1;
+                tkind = 1;
+            } else if (tpos < nr) {
+                cut = tpos;
+                tkind = __shfl_sync(FULL, anom ? 4 : (isend ? 2 : 3), tpos);
+                termpos = __shfl_sync(FULL, pos, tpos);
+                term_dp = __shfl_sync(FULL, dp, tpos);
+            } else {
+                cut = nr;
+            }
+            const unsigned below = cut >= 32 ? FULL : ((1u << cut) - 1u);
+            if (tkind != 4) {
+                const unsigned mb = qb & below;
+                const unsigned iw = __ballot_sync(FULL, inwin) & below;
+                const unsigned pb = iw & ~mb;
+                const int cnt = __popc(mb);
+                if (w == 0) {
+                    if ((pb >> lane) & 1u) {                // P events (position-ordered)
+                        const int e = nev + __popc(pb & lower);
+                        gw->ev_t[e] = tc;
+                        gw->ev_dp[e] = dp;
+                        gw->ev_pos[e] = pos;
+                        gw->ev_gap[e] = nmem + __popc(mb & lower);
+                    }
+                    if (cnt) {
+                        // members of this batch -> lanes nmem .. nmem+cnt-1
+                        double cbj = 0.0, cns = 0.0, civ = 0.0, cuq = 0.0, cnr = 0.0;
+                        int cj = 0;
+                        if ((mb >> lane) & 1u) {
+                            cbj = h->ci.beta; cns = h->ci.ns; civ = h->ci.inv; cuq = h->ci.u; cnr = h->ci.nr; cj = h->j;
+                        }
+                        const int bi = lane - nmem;
+                        const bool take = bi >= 0 && bi < cnt;
+                        const int src = take ? (int)__fns(mb, 0, bi + 1) : lane;
+                        const double x_tc = __shfl_sync(FULL, tc, src), x_dp = __shfl_sync(FULL, dp, src);
+                        const double x_bj = __shfl_sync(FULL, cbj, src), x_ns = __shfl_sync(FULL, cns, src);
+                        const double x_iv = __shfl_sync(FULL, civ, src), x_uq = __shfl_sync(FULL, cuq, src);
+                        const double x_nr = __shfl_sync(FULL, cnr, src);
+                        const int x_j = __shfl_sync(FULL, cj, src), x_pos = __shfl_sync(FULL, pos, src);
+                        if (take) {
+                            m_tc = x_tc; m_dp = x_dp; m_bj = x_bj; m_ns = x_ns; m_iv = x_iv; m_uq = x_uq; m_nr = x_nr;
+                            m_j = x_j; m_pos = x_pos;
+                        }
+                    }
+                }
+                // members' rows, one predicated pass (warp-uniform conditions)
+#pragma unroll
+                for (int b = 0; b < kGM; ++b) {
+                    if (b >= nmem && b < nmem + cnt) {
+                        const int ml = (int)__fns(mb, 0, b - nmem + 1);
+                        const SlotHdr* hm = reinterpret_cast<const SlotHdr*>(ring + (size_t)((k + ml) & kmask) * sbytes);
+                        const T* xs = reinterpret_cast<const T*>(hm + 1) + tid;
+#pragma unroll
+                        for (int q = 0; q < R; ++q) xw[b][q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
+                    }
+                }
+                nev += __popc(pb);
+                nmem += cnt;
+                ncand += __popc(iw);
+                if (iw) lastpos = __shfl_sync(FULL, pos, 31 - __clz(iw));
+            }
+            k += cut;
+            term = tkind;
+            __syncwarp();
+            if (lane == 0) st_rel_s(mycons_s, k);          // entries before k fully read
+        }
+        if (term == 4) {
+            // the producer's bound does not cover this window: restart at the
+            // window start under a larger drift hint (nothing was consumed yet)
+            ++gen;
+            if (w == 0) ++n_req;
+            if (tid == 0) {
+                cc->req_hint = __dadd_ru(Dq, __dmul_ru(2.0, Mg));
+                st_rel_s(reqp_s, wstart);
+                st_rel_s(reqg_s, gen);
+            }
+            continue;
+        }
+        // ---------------- all dots of the window, then one transposed butterfly ----------------
+        const long long c1 = clock64();
+        if (nmem > 0) {
+            double v[32];
+#pragma unroll
+            for (int b = 0; b < kGM; ++b) {
+                double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < R; q += 2) {
+                    a0 = fma(xw[b][q], rr[q], a0);
+                    if (q + 1 < R) a1 = fma(xw[b][q + 1], rr[q + 1], a1);
+                }
+                v[b] = a0 + a1;
+#pragma unroll
+                for (int b2 = 0; b2 < b; ++b2) {
+                    double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+                    for (int q = 0; q < R; q += 2) {
+                        g0 = fma(xw[b][q], xw[b2][q], g0);
+                        if (q + 1 < R) g1 = fma(xw[b][q + 1], xw[b2][q + 1], g1);
+                    }
+                    v[kGM + b * (b - 1) / 2 + b2] = g0 + g1;
+                }
+            }
+#pragma unroll
+            for (int i = kGDots; i < 32; ++i) v[i] = 0.0;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < o; ++i) {
+                    const double send = up ? v[i] : v[i + o];
+                    const double keep = up ? v[i + o] : v[i];
+                    v[i] = keep + __shfl_xor_sync(FULL, send, o);
+                }
+            }
+            gw->part[w][lane] = v[0];
+        }
+        named_bar(1, BT);
+        const long long c2 = clock64();
+        if (w == 0) {
+            // ---------------- the coordinate chain (warp 0; lanes redundant, branch-free) ----------------
+            double val = 0.0;
+            if (nmem > 0)
+                for (int q = 0; q < W; ++q) val += gw->part[q][lane];
+            double acc[kGM];
+#pragma unroll
+            for (int b = 0; b < kGM; ++b) acc[b] = __shfl_sync(FULL, val, b);
+            double Dl = D, gsl = gstep;
+            double my_d = 0.0, my_nb = 0.0, my_D = D, my_gs = gstep;   // lane b: member b's update / drift before it
+            unsigned procm = 0, nzm = 0;
+#pragma unroll
+            for (int b = 0; b < kGM; ++b) {
+                const double tc = __shfl_sync(FULL, m_tc, b), bj = __shfl_sync(FULL, m_bj, b);
+                const double ns = __shfl_sync(FULL, m_ns, b), iv = __shfl_sync(FULL, m_iv, b);
+                const double uq = __shfl_sync(FULL, m_uq, b), nr = __shfl_sync(FULL, m_nr, b);
+                if (lane == b) { my_D = Dl; my_gs = gsl; }
+                const bool run = b < nmem && (!use_t || !(Dl < tc));     // certified members: zero update
+                const double g = acc[b];
+                const double q0 = g * iv;
+                const double rq = fma(-q0, ns, g);
+                const double qq = fma(rq, iv, q0);            // RN(g / nsq)
+                const double z = bj + qq;
+                const double nb = z > uq ? z - uq : (z < -uq ? z + uq : 0.0);
+                const double d = run ? nb - bj : 0.0;
+                procm |= run ? (1u << b) : 0u;
+                if (d != 0.0) {
+                    nzm |= 1u << b;
+#pragma unroll
+                    for (int b2 = b + 1; b2 < kGM; ++b2)
+                        acc[b2] = fma(-d, __shfl_sync(FULL, val, kGM + b2 * (b2 - 1) / 2 + b), acc[b2]);
+                    if (use_t) {
+                        const double step = __dmul_ru(fabs(d), nr);
+                        Dl = delta_step_g(Dl, step, rho0);
+                        gsl = 0.875 * gsl + 0.125 * step;
+                    }
+                }
+                if (lane == b) { my_d = d; my_nb = nb; }
+            }
+            if (lane == nmem) { my_D = Dl; my_gs = gsl; }            // trailing gap
+            // ---- violations, resolved by position: discard (a bound no longer covers D)
+            // or truncate (a P position lost its certificate) at the first one
+            int kd = 0x7fffffff, kt = 0x7fffffff;
+            if (use_t) {
+                if (lane < nmem && my_D > m_dp) kd = m_pos;
+                for (int e0 = 0; e0 < nev; e0 += 32) {
+                    const int e = e0 + lane;
+                    const int gp = e < nev ? gw->ev_gap[e] : 0;
+                    const double De = __shfl_sync(FULL, my_D, gp);
+                    if (e < nev) {
+                        const int ps = gw->ev_pos[e];
+                        if (De > gw->ev_dp[e]) kd = min(kd, ps);
+                        else if (!(De < gw->ev_t[e])) kt = min(kt, ps);
+                    }
+                }
+                kd = __reduce_min_sync(FULL, kd);
+                kt = __reduce_min_sync(FULL, kt);
+                if (term == 2 && Dl > term_dp) kd = min(kd, m);
+            }
+            int action = 0, ncommit = nmem, rpos = 0;
+            double vio = Dl;
+            if (kd != 0x7fffffff && kd <= kt) {
+                action = 2;
+                vio = Dl;
+                ncommit = 0;
+            } else if (kt != 0x7fffffff) {
+                action = 1;
+                rpos = kt;
+                ncommit = __popc(__ballot_sync(FULL, lane < nmem && m_pos < kt));
+                Dl = __shfl_sync(FULL, my_D, ncommit);
+                gsl = __shfl_sync(FULL, my_gs, ncommit);
+            }
+            if (action == 2) { Dl = D; gsl = gstep; }
+            // ---- commit
+            int done = 0, nws = wstart;
+            if (action == 0) {
+                if (term == 2) done = 1;
+                else nws = lastpos >= 0 ? lastpos + 1 : termpos;
+            } else {
+                ++gen;
+                ++n_req;
+                nws = action == 1 ? rpos : wstart;
+                if (lane == 0) {
+                    const double mg2 = __dmul_ru(2.0 * kGM, gsl);
+                    cc->req_hint = action == 2 ? __dadd_ru(vio, mg2) : __dadd_ru(Dl, mg2);
+                    st_rel_s(reqp_s, nws);
+                    st_rel_s(reqg_s, gen);
+                }
+            }
+            const unsigned cm = (1u << ncommit) - 1u;
+            n_unc += __popc(procm & cm);
+            n_nz += __popc(nzm & cm);
+            n_skip += ncommit - __popc(procm & cm);
+            n_cand += ncand;
+            if (lane < kGM) gw->dres[lane] = (lane < ncommit) ? my_d : 0.0;
+            if (lane < ncommit && ((nzm >> lane) & 1u)) {
+                P.beta[m_j] = my_nb;
+                P.cinfo[m_j].beta = my_nb;
+                if (use_t && m_bj == 0.0) {
+                    P.t[m_pos] = -1.0f;                      // now in the support
+                    if (m <= kTTile) ts[m_pos] = -1.0f;      // resident tile (single tile only)
+                }
+            }
+            if (lane == 0) {
+                gw->ncommit = ncommit;
+                gw->D = Dl;
+                gw->gstep = gsl;
+                gw->gen = gen;
+                gw->wstart = nws;
+                gw->done = done;
+                st_vol_f64_s(dpub_s, Dl);
+                if (done) st_rel_s(fin_s, 1);
+            }
+        }
+        named_bar(1, BT);
+        const long long c3 = clock64();
+        const int nc = gw->ncommit;
+#pragma unroll
+        for (int b = 0; b < kGM; ++b) {
+            if (b < nc) {
+                const double d = gw->dres[b];
+                if (d != 0.0) {
+#pragma unroll
+                    for (int q = 0; q < R; ++q) rr[q] = __dsub_rn(rr[q], __dmul_rn(d, xw[b][q]));
+                }
+            }
+        }
+        D = gw->D;
+        gstep = gw->gstep;
+        gen = gw->gen;
+        wstart = gw->wstart;
+        if (P.cd_prof && tid == 0) {
+            SolveCtl* c = P.ctl;
+            const long long c4 = clock64();
+            c->c_form += c1 - c0 - cw; c->c_wait += cw; c->c_red += c2 - c1; c->c_chain += c3 - c2; c->c_upd += c4 - c3;
+            c->n_win += 1; c->n_mem += nmem;
+        }
+        if (gw->done) break;
+    }
+}
+
 __host__ __device__ inline int cd_ring_slots(int64_t ld, int es) {
     // power of two, at most 64 slots and ~128 KB of ring
     const int64_t bytes = ld * es + 80;
@@ -677,7 +1059,7 @@ __host__ __device__ inline size_t cd_slot_bytes(int64_t ld, int es) {
     return sizeof(SlotHdr) + (size_t)ld * es;          // ld * es is a multiple of 16
 }
 __host__ __device__ inline size_t cd_smem_bytes_rt(int64_t ld, int es) {
-    return (size_t)kTTile * (sizeof(float) + sizeof(int32_t)) + 64 * sizeof(double) + sizeof(CdCtl) +
+    return (size_t)kTTile * (sizeof(float) + sizeof(int32_t)) + 64 * sizeof(double) + sizeof(CdCtl) + sizeof(GWin) +
            (size_t)cd_ring_slots(ld, es) * cd_slot_bytes(ld, es);
 }
 
@@ -692,7 +1074,8 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     int32_t* As = reinterpret_cast<int32_t*>(smem + kTTile * sizeof(float));
     double* part = reinterpret_cast<double*>(smem + kTTile * (sizeof(float) + sizeof(int32_t)));   // [2][32]
     CdCtl* cc = reinterpret_cast<CdCtl*>(part + 64);
-    unsigned char* ring = reinterpret_cast<unsigned char*>(cc + 1);
+    GWin* gw = reinterpret_cast<GWin*>(cc + 1);
+    unsigned char* ring = reinterpret_cast<unsigned char*>(gw + 1);
     const int K = cd_ring_slots(P.ld, (int)sizeof(T));          // power of two
     const int kmask = K - 1, kshift = __ffs(K) - 1;
     const unsigned sbytes = (unsigned)cd_slot_bytes(P.ld, (int)sizeof(T));
@@ -706,11 +1089,12 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     }
     // ---- setup (all threads)
     if (tid == 0) {
-        for (int s = 0; s < K; ++s) { mbar_init(&cc->bar[s], 1); cc->data_ready[s] = 0; }
+        for (int s = 0; s < K; ++s) mbar_init(&cc->bar[s], 1);
         for (int k = 0; k < 8; ++k) cc->consumed[k] = 0;
         cc->dpub = use_t ? ctl->cd_delta : 0.0;
         cc->req_gen = 0;
         cc->req_pos = 0;
+        cc->req_hint = 0.0;
         cc->finished = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -726,20 +1110,39 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     const unsigned ring_s = smem_u32(ring);
     const unsigned bar_s = smem_u32(&cc->bar[0]);
     // control words as 32-bit shared addresses, computed once
-    const unsigned dat_s = smem_u32(&cc->data_ready[0]);
     const unsigned cons_s = smem_u32(&cc->consumed[0]), fin_s = smem_u32(&cc->finished);
     const unsigned reqg_s = smem_u32(&cc->req_gen), reqp_s = smem_u32(&cc->req_pos);
     const unsigned dpub_s = smem_u32(&cc->dpub);
 
-    if (w == W && W < (int)(blockDim.x >> 5)) {
+    // warp roles: the W compute warps take the TOP warp ids and the producer
+    // the one below them.  The scheduler of each SMSP (warps w, w+4) issues
+    // the highest eligible warp id first, so the serial chain (compute warp 0)
+    // never loses an issue slot to the spinning producer.
+    const int wbase = (int)(blockDim.x >> 5) - W;
+    if (w == wbase - 1) {
         // =================== producer warp ===================
+        // Entries are published through the slot mbarriers themselves: the
+        // header is written before the arrive (release), the column bytes
+        // complete the phase (complete_tx), and consumers test the phase of
+        // entry e (parity (e / K) & 1) lane-parallel.  Entry e is issued only
+        // after entry e - K was consumed by every compute warp, so a phase is
+        // never tested more than one use ahead.
         const T* __restrict__ X = (const T*)P.X;
         const ColInfo* __restrict__ cinfo = P.cinfo;
         const double gs0 = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * P.lam;
-        const double margin_gs = __dmul_ru(2.0 * K, gs0);
+        // Gram windows (cd_gram): candidates are selected under dpub + 6 Mg, and
+        // carry column bytes only when t <= dpub + 4 Mg (Mg = the consumer's
+        // window-growth allowance); the rest are header-only entries whose
+        // certification the consumer re-checks at their turn.
+        const bool gram = P.cd_gram != 0;
+        const double mg0 = __dmul_ru((double)kGM, gs0);
+        const double margin_gs = gram ? __dmul_ru(6.0, mg0) : __dmul_ru(2.0 * K, gs0);
+        const double margin_dat = __dmul_ru(4.0, mg0);
+        const unsigned FULL = 0xffffffffu;
+        double hint = 0.0;
         int tb = 0, tend = min(m, kTTile);
         int qnext = 0, gen = 0;
-        int k_issue = 0, k_data = 0;       // entries issued / data published
+        int k_issue = 0;
         bool done = false;
         unsigned long long t0 = gtimer();       // reset on progress (watchdog)
         auto load_tile_p = [&](int from) {
@@ -748,117 +1151,110 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
             for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
             __syncwarp();
         };
-        // every control word is read by lane 0 and broadcast: the warp must take
-        // uniform decisions (ballots and shuffles below use the full mask)
-        auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
-        while (!bcast(lane == 0 ? ld_acq_s(fin_s) : 0)) {
-            // restart request from the compute warps
-            const int rg = bcast(lane == 0 ? ld_acq_s(reqg_s) : 0);
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // cinfo/beta stores before TMA reads
+        while (true) {
+            // control words: lane 0 fin, lane 1 restart generation, lanes 2.. consumed counters
+            int cw = 0;
+            if (lane == 0) cw = ld_acq_s(fin_s);
+            else if (lane == 1) cw = ld_acq_s(reqg_s);
+            else if (lane < 2 + W) cw = ld_acq_s(cons_s + 4u * (lane - 2));
+            if (__shfl_sync(FULL, cw, 0)) break;
+            const int rg = __shfl_sync(FULL, cw, 1);
+            const int cmin = __reduce_min_sync(FULL, (lane >= 2 && lane < 2 + W) ? cw : 0x7fffffff);
             if (rg != gen) {
                 gen = rg;
-                const int rp = bcast(lane == 0 ? ld_acq_s(reqp_s) : 0);
+                const int rp = __shfl_sync(FULL, lane == 0 ? ld_acq_s(reqp_s) : 0, 0);
+                double hv = lane == 0 ? cc->req_hint : 0.0;
+                hint = __shfl_sync(FULL, hv, 0);
                 if (rp < tb || rp > tend || (rp == tend && tend < m)) load_tile_p(rp);
                 qnext = rp;
                 done = false;
             }
-            // data readiness, in order
-            while (k_data < k_issue) {
-                const int s = k_data & kmask;
-                int ok = 0;
-                if (lane == 0) ok = mbar_test_s(bar_s + 8u * s, (unsigned)((k_data >> kshift) & 1));
-                ok = __shfl_sync(0xffffffffu, ok, 0);
-                if (!ok) break;
-                if (lane == 0) st_rel_s(dat_s + 4u * s, k_data + 1);
-                ++k_data;
-                t0 = gtimer();
-            }
-            // free slots: entries consumed by every compute warp and whose bytes landed
-            int cmin = 0x7fffffff;
-            if (lane == 0)
-                for (int q = 0; q < W; ++q) cmin = min(cmin, ld_acq_s(cons_s + 4u * q));
-            cmin = bcast(cmin);
-            const int free_slots = min(K - (k_issue - cmin), K - (k_issue - k_data));
+            int free_slots = K - (k_issue - cmin);
             if (done || free_slots <= 0) {
                 __nanosleep(32);
-                spin_guard(t0, 1, k_issue, k_data, cmin, (int)done);
+                spin_guard(t0, 1, k_issue, cmin, gen, (int)done);
                 continue;
             }
-            // one ballot: every candidate of the next window
+            t0 = gtimer();
             double dpub = lane == 0 ? ld_vol_f64_s(dpub_s) : 0.0;
-            dpub = __shfl_sync(0xffffffffu, dpub, 0);
-            const double dp = use_t ? __dadd_ru(dpub, margin_gs) : 0.0;
+            dpub = __shfl_sync(FULL, dpub, 0);
+            const double dp = use_t ? fmax(__dadd_ru(dpub, margin_gs), hint) : 0.0;
+            const double dd = fmax(__dadd_ru(dpub, margin_dat), hint);   // column bytes for t <= dd (gram)
+            // scan and issue until the free slots are used or the epoch ends
             int base = qnext;
-            unsigned mask = 0;
-            while (true) {
+            while (free_slots > 0) {
                 if (base >= tend) {
-                    if (tend >= m) break;
+                    if (tend >= m) {
+                        // end of the epoch: an entry without data
+                        if (lane == 0) {
+                            const int s = k_issue & kmask;
+                            SlotHdr* h = reinterpret_cast<SlotHdr*>(ring + (size_t)s * sbytes);
+                            h->pos = m;
+                            h->gen = gen;
+                            h->dp = dp;                        // positions after the last candidate: certified under dp
+                            h->flags = kNoData;
+                            mbar_arrive_s(bar_s + 8u * s);     // release: the header is visible with the phase
+                        }
+                        ++k_issue;
+                        done = true;
+                        break;
+                    }
                     load_tile_p(tend);
                     base = tb;
                     continue;
                 }
                 const int q = base + lane;
                 const bool unc = q < tend && (!use_t || !(dp < (double)ts[q - tb]));
-                mask = __ballot_sync(0xffffffffu, unc);
-                if (mask) break;
-                base += 32;
-            }
-            // keep at most free_slots candidates (lowest positions first)
-            const int navail = min(__popc(mask), free_slots);
-            if (navail > 0) {
-                const unsigned lower = (lane == 0) ? 0u : (mask & ((1u << lane) - 1u));
-                const int rank = __popc(lower);
-                const bool mine = ((mask >> lane) & 1u) && rank < navail;
-                if (mine) {
+                const unsigned mask = __ballot_sync(FULL, unc);
+                if (!mask) { base += 32; continue; }
+                const int navail = min(__popc(mask), free_slots);
+                const int rank = __popc(mask & ((1u << lane) - 1u));
+                if (((mask >> lane) & 1u) && rank < navail) {
                     const int p = base + lane;
-                    const int k = k_issue + rank;
-                    const int s = k & kmask;
+                    const int s = (k_issue + rank) & kmask;
                     const int32_t j = As[p - tb];
                     const unsigned slot = ring_s + (unsigned)s * sbytes;
-                    const unsigned b = bar_s + 8u * s;
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_expect_tx_s(b, xbytes + (unsigned)sizeof(ColInfo));
-                    tma_bulk_g2s_s(slot + (unsigned)sizeof(SlotHdr), X + (int64_t)j * P.ld, xbytes, b);
-                    tma_bulk_g2s_s(slot, cinfo + j, (unsigned)sizeof(ColInfo), b);
+                    const unsigned bb = bar_s + 8u * s;
+                    const double tcp = (double)ts[p - tb];
+                    const bool nodata = gram && use_t && dd < tcp;
                     SlotHdr* h = reinterpret_cast<SlotHdr*>(ring + (size_t)s * sbytes);
-                    h->tcert = (double)ts[p - tb];
+                    h->tcert = tcp;
                     h->dp = dp;
                     h->pos = p;
                     h->j = j;
                     h->gen = gen;
+                    h->flags = nodata ? kNoData : 0;
+                    if (nodata) {
+                        mbar_arrive_s(bb);                     // header only: completes the phase at once
+                    } else {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        mbar_expect_tx_s(bb, xbytes + (unsigned)sizeof(ColInfo));
+                        tma_bulk_g2s_s(slot + (unsigned)sizeof(SlotHdr), X + (int64_t)j * P.ld, xbytes, bb);
+                        tma_bulk_g2s_s(slot, cinfo + j, (unsigned)sizeof(ColInfo), bb);
+                    }
                 }
-                // position of the last issued candidate (rank navail-1)
-                int lastbit = 0;
-                {
-                    unsigned mm = mask;
-                    for (int r = 0; r < navail - 1; ++r) mm &= mm - 1;
-                    lastbit = __ffs(mm) - 1;
-                }
+                const int lastbit = (int)__fns(mask, 0, navail);
                 qnext = base + lastbit + 1;
+                base = qnext;
                 k_issue += navail;
-            } else if (mask == 0 && base >= tend && tend >= m) {
-                // end of the epoch: an entry without data (plain arrive completes the phase)
-                if (lane == 0) {
-                    const int s = k_issue & kmask;
-                    SlotHdr* h = reinterpret_cast<SlotHdr*>(ring + (size_t)s * sbytes);
-                    h->pos = m;
-                    h->gen = gen;
-                    mbar_arrive_s(bar_s + 8u * s);
-                }
-                ++k_issue;
-                done = true;
+                free_slots -= navail;
             }
             __syncwarp();
         }
-        // drain outstanding transactions before the ring memory is reused
-        while (k_data < k_issue) {
-            const int s = k_data & kmask;
-            int ok = 0;
-            if (lane == 0) ok = mbar_test_s(bar_s + 8u * s, (unsigned)((k_data >> kshift) & 1));
-            ok = __shfl_sync(0xffffffffu, ok, 0);
-            if (ok) ++k_data; else spin_guard(t0, 2, k_issue, k_data, 0, 0);
+        // drain outstanding transactions before the ring memory is reused:
+        // the last min(K, k_issue) entries, one per slot
+        {
+            const int e = k_issue - 1 - lane;
+            bool pend = lane < K && e >= 0;
+            while (__any_sync(FULL, pend)) {
+                if (pend && mbar_test_s(bar_s + 8u * (e & kmask), (unsigned)((e >> kshift) & 1))) pend = false;
+                spin_guard(t0, 2, k_issue, 0, 0, 0);
+            }
         }
-    } else if (w < W) {
+    } else if (w >= wbase) {
         // =================== compute warps ===================
+        const int tid = threadIdx.x - 32 * wbase, w = tid >> 5;     // index within the compute group
         double rr[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) { const int r = tid + k * BT; rr[k] = r < n ? P.rho[r] : 0.0; }
@@ -872,12 +1268,17 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
         int n_unc = 0, n_nz = 0, n_req = 0, n_cand = 0, n_skip = 0;
         const int cmask = min(7, (K >> 2) - 1);     // consumed is signalled every cmask+1 entries
         const unsigned mycons_s = cons_s + 4u * w;
+        if (P.cd_gram)
+            cd_consume_gram<T, R>(P, m, W, ring, sbytes, kmask, bar_s, kshift, cons_s, fin_s, reqg_s, reqp_s, dpub_s, cc, gw, ts,
+                                  use_t, rho0, rr, D, gstep, n_unc, n_nz, n_req, n_cand, n_skip, tid);
+        else
         for (int k = 0;; ++k) {
             const int s = k & kmask;
             // one poll per entry: header and bytes are published together (in order)
-            if (ld_acq_s(dat_s + 4u * s) != k + 1) {
+            const unsigned par = (unsigned)((k >> kshift) & 1);
+            if (!mbar_test_s(bar_s + 8u * s, par)) {
                 const unsigned long long t0 = gtimer();
-                while (ld_acq_s(dat_s + 4u * s) != k + 1) spin_guard(t0, 4, k, ld_acq_s(dat_s + 4u * s), gen, last);
+                while (!mbar_test_s(bar_s + 8u * s, par)) spin_guard(t0, 4, k, gen, last, 0);
             }
             const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
             const int pos = h->pos;
@@ -1594,6 +1995,10 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
         ctl->converged = 1;
     }
     if (g.c == 0 && threadIdx.x == 0) { ctl->done = 1; ctl->k = k; }
+    if (P.cd_prof && g.c == 0 && threadIdx.x == 0 && ctl->n_win)
+        printf("cdprof lam=%.6e windows=%llu members=%llu cyc/win: form=%.0f wait=%.0f red=%.0f chain=%.0f upd=%.0f\n", P.lam,
+               ctl->n_win, ctl->n_mem, (double)ctl->c_form / ctl->n_win, (double)ctl->c_wait / ctl->n_win,
+               (double)ctl->c_red / ctl->n_win, (double)ctl->c_chain / ctl->n_win, (double)ctl->c_upd / ctl->n_win);
     (void)broke;
 }
 

@@ -42,9 +42,15 @@ def test_path_cfg0_full():
     assert np.all(ra.converged)
 
 
-def test_path_no_certify_identical_to_certify():
-    """Certified-zero skipping is exact: with and without it the GPU path is
-    bit-identical."""
+@pytest.mark.parametrize("gram", ["0", "1"])
+def test_path_no_certify_identical_to_certify(gram, monkeypatch):
+    """Certified-zero skipping is exact.  With one reduction per coordinate
+    (GS_CD_GRAM=0) the paths with and without it are bit-identical.  The
+    Gram-window consumer groups the coordinates it computes into windows, so
+    skipping changes the window partition and hence roundings (never an
+    update): epochs, traces' active-set sizes and supports are identical and
+    the coefficients agree to round-off."""
+    monkeypatch.setenv("GS_CD_GRAM", gram)
     c = synth.cfg0(p=800)
     X = gs.DesignMatrix(c.X)
     dev = gs.DeviceSolver(X, c.y)
@@ -52,9 +58,25 @@ def test_path_no_certify_identical_to_certify():
     a = gs.run_path(X, c.y, grid, gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000), solver=dev)
     b = gs.run_path(X, c.y, grid, gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000, certify=False),
                     solver=dev)
-    assert np.array_equal(a.betas, b.betas)
-    assert [x.gap for x in a.certs] == [x.gap for x in b.certs]
-    assert a.traces == b.traces
+    if gram == "0":
+        assert np.array_equal(a.betas, b.betas)
+        assert [x.gap for x in a.certs] == [x.gap for x in b.certs]
+        assert a.traces == b.traces
+    else:
+        assert [s.passes_done for s in a.states] == [s.passes_done for s in b.states]
+        assert [[r[:2] for r in t] for t in a.traces] == [[r[:2] for r in t] for t in b.traces]
+        assert np.array_equal(a.betas != 0, b.betas != 0)
+        np.testing.assert_allclose(a.betas, b.betas, rtol=0, atol=1e-12 * np.abs(b.betas).max())
+
+
+@pytest.mark.parametrize("gram", ["0", "1"])
+def test_path_cd_modes_match_oracle(gram, monkeypatch):
+    """Both CD consumers (Gram windows, one reduction per coordinate) meet the
+    parity criteria against the oracle on the cfg0 generator."""
+    monkeypatch.setenv("GS_CD_GRAM", gram)
+    c = synth.cfg0(p=2000)
+    ra, rb, yy = _paths(c.X, c.y, 25, 3.0, c.epsilon)
+    compare_paths(ra, rb, yy)
 
 
 def test_path_deterministic_bit_identical():
