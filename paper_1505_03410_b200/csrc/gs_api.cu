@@ -491,13 +491,14 @@ static CdShape cd_shape(int64_t n) {
     if (n <= 64) return {2, 1};
     if (n <= 512) return {4, (int)((n + 127) / 128)};
     if (n <= 1792) return {8, (int)((n + 255) / 256)};
+    if (n <= 10752) return {48, (int)((n + 1535) / 1536)};     // cfg2 (n = 10000): rho rows in registers, columns streamed
     return {0, 0};
 }
 
 // CD consumer per shape (measured on B200, profiles/r01/cd_modes.md): Gram
-// windows win while the member rows fit 4 per lane (cfg0: 10.8 s vs 12.9 s);
-// at 8 rows per lane (cfg1) one reduction per coordinate is faster.
-static int cd_gram_default(int64_t n) { return cd_shape(n).R <= 4 ? 1 : 0; }
+// windows win only for a single-warp chain (cfg0: 10.8 s vs 12.9 s); with a
+// cross-warp reduction per coordinate (cfg1, cfg4) the direct chain is faster.
+static int cd_gram_default(int64_t n) { return (cd_shape(n).R <= 4 && cd_shape(n).W == 1) ? 1 : 0; }
 
 static int launch_solve(const gs_matrix* M, cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem,
                         int R) {
@@ -534,7 +535,7 @@ static int check_shape(const gs_matrix* M) {
         if (solve_smem(M) > 225 * 1024) return fail(GS_ERR_VALUE, "sparse solver supports n <= 22400 in this build");
         return GS_OK;
     }
-    if (cd_shape(M->n).R == 0) return fail(GS_ERR_VALUE, "dense solver supports n <= 1792 in this build");
+    if (cd_shape(M->n).R == 0) return fail(GS_ERR_VALUE, "dense solver supports n <= 10752 in this build");
     return GS_OK;
 }
 
@@ -1156,7 +1157,7 @@ extern "C" int gs_batch_create(const gs_matrix* X0, const double* y0, const int3
         Bt->ld = (n + align - 1) / align * align;
         Bt->ldy = n + 2;
         Bt->shape.n = n; Bt->shape.p = X0->p; Bt->shape.ld = Bt->ld; Bt->shape.dtype = X0->dtype;
-        if (cd_shape(n).R == 0) return fail(GS_ERR_VALUE, "batched solver supports n <= 1792");
+        if (cd_shape(n).R == 0 || cd_shape(n).R > 8) return fail(GS_ERR_VALUE, "batched solver supports n <= 1792");
         const int64_t p = Bt->p, ld = Bt->ld;
         const size_t es = X0->dtype == GS_DTYPE_F64 ? 8 : 4;
         CK(cudaStreamCreateWithFlags(&Bt->st, cudaStreamNonBlocking));

@@ -601,7 +601,9 @@ static __device__ void cta_post(const SolveDev& P, double* red) {
 // ---------------------------------------------------------------------------
 // CD epoch, dense, run by the first W warps of CTA 0
 // ---------------------------------------------------------------------------
-constexpr int kTTile = 8192;   // certification thresholds staged per tile (float)
+constexpr int kTTile = 8192;   // certification thresholds staged per tile (float), columns <= 16 KB
+// threshold-tile length: halved for long columns so the TMA column ring keeps 4 slots
+__host__ __device__ inline int cd_tile(int64_t ld, int es) { return ld * es > 16384 ? kTTile / 2 : kTTile; }
 
 static __device__ __forceinline__ int64_t scan_tile(const float* ts, int64_t tb, int64_t tend, int64_t from, double D,
                                              int lane) {
@@ -1007,7 +1009,7 @@ static __device__ __forceinline__ void cd_consume_gram(const SolveDev& P, const 
                 P.cinfo[m_j].beta = my_nb;
                 if (use_t && m_bj == 0.0) {
                     P.t[m_pos] = -1.0f;                      // now in the support
-                    if (m <= kTTile) ts[m_pos] = -1.0f;      // resident tile (single tile only)
+                    if (m <= cd_tile(P.ld, (int)sizeof(T))) ts[m_pos] = -1.0f;      // resident tile (single tile only)
                 }
             }
             if (lane == 0) {
@@ -1059,7 +1061,7 @@ __host__ __device__ inline size_t cd_slot_bytes(int64_t ld, int es) {
     return sizeof(SlotHdr) + (size_t)ld * es;          // ld * es is a multiple of 16
 }
 __host__ __device__ inline size_t cd_smem_bytes_rt(int64_t ld, int es) {
-    return (size_t)kTTile * (sizeof(float) + sizeof(int32_t)) + 64 * sizeof(double) + sizeof(CdCtl) + sizeof(GWin) +
+    return (size_t)cd_tile(ld, es) * (sizeof(float) + sizeof(int32_t)) + 64 * sizeof(double) + sizeof(CdCtl) + sizeof(GWin) +
            (size_t)cd_ring_slots(ld, es) * cd_slot_bytes(ld, es);
 }
 
@@ -1071,8 +1073,9 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     const int BT = W * 32;
     const int m = (int)m64;
     float* ts = reinterpret_cast<float*>(smem);
-    int32_t* As = reinterpret_cast<int32_t*>(smem + kTTile * sizeof(float));
-    double* part = reinterpret_cast<double*>(smem + kTTile * (sizeof(float) + sizeof(int32_t)));   // [2][32]
+    const int TT = cd_tile(P.ld, (int)sizeof(T));
+    int32_t* As = reinterpret_cast<int32_t*>(smem + TT * sizeof(float));
+    double* part = reinterpret_cast<double*>(smem + TT * (sizeof(float) + sizeof(int32_t)));   // [2][32]
     CdCtl* cc = reinterpret_cast<CdCtl*>(part + 64);
     GWin* gw = reinterpret_cast<GWin*>(cc + 1);
     unsigned char* ring = reinterpret_cast<unsigned char*>(gw + 1);
@@ -1098,9 +1101,9 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
         cc->finished = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const bool keep_tile = (m <= kTTile) && *tile_valid;
+    const bool keep_tile = (m <= TT) && *tile_valid;
     if (!keep_tile) {
-        const int lim = min(m, kTTile);
+        const int lim = min(m, TT);
         for (int q = tid; q < lim; q += blockDim.x) {
             As[q] = P.A[q];
             ts[q] = use_t ? P.t[q] : -1.0f;
@@ -1140,14 +1143,14 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
         const double margin_dat = __dmul_ru(4.0, mg0);
         const unsigned FULL = 0xffffffffu;
         double hint = 0.0;
-        int tb = 0, tend = min(m, kTTile);
+        int tb = 0, tend = min(m, TT);
         int qnext = 0, gen = 0;
         int k_issue = 0;
         bool done = false;
         unsigned long long t0 = gtimer();       // reset on progress (watchdog)
         auto load_tile_p = [&](int from) {
-            tb = (from / kTTile) * kTTile;
-            tend = min(m, tb + kTTile);
+            tb = (from / TT) * TT;
+            tend = min(m, tb + TT);
             for (int q = tb + lane; q < tend; q += 32) { As[q - tb] = P.A[q]; ts[q - tb] = use_t ? P.t[q] : -1.0f; }
             __syncwarp();
         };
@@ -1268,13 +1271,18 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
         int n_unc = 0, n_nz = 0, n_req = 0, n_cand = 0, n_skip = 0;
         const int cmask = min(7, (K >> 2) - 1);     // consumed is signalled every cmask+1 entries
         const unsigned mycons_s = cons_s + 4u * w;
-        if (P.cd_gram)
-            cd_consume_gram<T, R>(P, m, W, ring, sbytes, kmask, bar_s, kshift, cons_s, fin_s, reqg_s, reqp_s, dpub_s, cc, gw, ts,
-                                  use_t, rho0, rr, D, gstep, n_unc, n_nz, n_req, n_cand, n_skip, tid);
-        else
+        bool gram = false;
+        if constexpr (R <= 8) gram = P.cd_gram != 0;     // member rows held in registers: R <= 8 only
+        if (gram) {
+            if constexpr (R <= 8)
+                cd_consume_gram<T, R>(P, m, W, ring, sbytes, kmask, bar_s, kshift, cons_s, fin_s, reqg_s, reqp_s, dpub_s, cc,
+                                      gw, ts, use_t, rho0, rr, D, gstep, n_unc, n_nz, n_req, n_cand, n_skip, tid);
+        } else
         for (int k = 0;; ++k) {
             const int s = k & kmask;
-            // one poll per entry: header and bytes are published together (in order)
+            // entries before k are fully read: consumed is signalled in batches (release store)
+            if (k > 0 && (k & cmask) == 0) { __syncwarp(); if (lane == 0) st_rel_s(mycons_s, k); }
+            // one poll per entry: header and bytes are published together through the slot mbarrier
             const unsigned par = (unsigned)((k >> kshift) & 1);
             if (!mbar_test_s(bar_s + 8u * s, par)) {
                 const unsigned long long t0 = gtimer();
@@ -1284,26 +1292,18 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
             const int pos = h->pos;
             const int hg = h->gen;
             const double tc = h->tcert, dp = h->dp;
-            const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
-            const int32_t j = h->j;
-            const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
-            double xv[R];
-#pragma unroll
-            for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
-            // consumed is signalled in batches (release store; the slot is fully read)
-            if ((k & cmask) == cmask) { __syncwarp(); if (lane == 0) st_rel_s(mycons_s, k + 1); }
             bool process = hg == gen && pos < m;
-            if (process && use_t) {
-                if (D > dp) {
-                    // drift outgrew the queue's bound: restart after the last processed position
-                    ++n_req;
-                    ++gen;
-                    if (tid == 0) { st_rel_s(reqp_s, last + 1); st_rel_s(reqg_s, gen); }
-                    process = false;
-                } else if (D < tc) {
-                    ++n_skip;                              // certified: zero update
-                    process = false;
-                }
+            if (hg == gen && use_t && D > dp) {
+                // drift outgrew the queue's bound (for the end entry: the positions
+                // after the last candidate): restart after the last processed position
+                ++n_req;
+                ++gen;
+                if (tid == 0) { st_rel_s(reqp_s, last + 1); st_rel_s(reqg_s, gen); }
+                continue;
+            }
+            if (process && use_t && D < tc) {
+                ++n_skip;                              // certified: zero update
+                process = false;
             }
             if (!process) {
                 if (hg == gen && pos >= m) {
@@ -1314,14 +1314,37 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 continue;
             }
             ++n_cand;
+            const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
+            const int32_t j = h->j;
+            const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
             // ---- critical chain
-            double a0 = 0.0, a1 = 0.0;
+            constexpr int RX = R <= 8 ? R : 1;
+            double xv[RX];
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if constexpr (R <= 8) {
 #pragma unroll
-            for (int q = 0; q < R; q += 2) {
-                a0 = fma(xv[q], rr[q], a0);
-                if (q + 1 < R) a1 = fma(xv[q + 1], rr[q + 1], a1);
+                for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
+#pragma unroll
+                for (int q = 0; q < R; q += 2) {
+                    a0 = fma(xv[q], rr[q], a0);
+                    if (q + 1 < R) a1 = fma(xv[q + 1], rr[q + 1], a1);
+                }
+            } else {
+                // long columns: stream the slot from shared memory (4 independent chains)
+#pragma unroll
+                for (int q = 0; q < R; q += 4) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double x = (q + u < R && tid + (q + u) * BT < n) ? to_d(xs[(q + u) * BT]) : 0.0;
+                        const double r = q + u < R ? rr[q + u] : 0.0;
+                        if (u == 0) a0 = fma(x, r, a0);
+                        else if (u == 1) a1 = fma(x, r, a1);
+                        else if (u == 2) a2 = fma(x, r, a2);
+                        else a3 = fma(x, r, a3);
+                    }
+                }
             }
-            double acc = warp_sum(a0 + a1);
+            double acc = warp_sum((a0 + a1) + (a2 + a3));
             double g;
             if (W > 1) {
                 if (lane == 0) part[pb * 32 + w] = acc;
@@ -1342,8 +1365,14 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
             last = pos;
             if (d != 0.0) {
                 ++n_nz;
+                if constexpr (R <= 8) {
 #pragma unroll
-                for (int q = 0; q < R; ++q) rr[q] = __dsub_rn(rr[q], __dmul_rn(d, xv[q]));
+                    for (int q = 0; q < R; ++q) rr[q] = __dsub_rn(rr[q], __dmul_rn(d, xv[q]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < R; ++q)
+                        rr[q] = __dsub_rn(rr[q], __dmul_rn(d, (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0));
+                }
                 if (use_t) {
                     const double step = __dmul_ru(fabs(d), nr);
                     D = delta_step(D, step, rho0);
@@ -1355,7 +1384,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 cinfo_w[j].beta = nb;
                 if (use_t && bj == 0.0) {
                     tg[pos] = -1.0f;                       // now in the support
-                    if (m <= kTTile) ts[pos] = -1.0f;      // resident tile (single tile only)
+                    if (m <= TT) ts[pos] = -1.0f;      // resident tile (single tile only)
                 }
                 st_vol_f64_s(dpub_s, D);
             }
@@ -1391,7 +1420,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
     }
     __syncthreads();
     if (tid == 0) {
-        *tile_valid = (m <= kTTile) ? 1 : 0;
+        *tile_valid = (m <= TT) ? 1 : 0;
         for (int s = 0; s < K; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&cc->bar[s])) : "memory");
     }
     __syncthreads();

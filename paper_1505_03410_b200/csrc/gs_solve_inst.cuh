@@ -46,7 +46,8 @@ cudaError_t GS_CAT(gs_launch_solve_, GS_SUF)(int R, cudaStream_t st, const Solve
         case 1: return solve_R<1>(st, dprobs, G, nprob, smem);
         case 2: return solve_R<2>(st, dprobs, G, nprob, smem);
         case 4: return solve_R<4>(st, dprobs, G, nprob, smem);
-        default: return solve_R<8>(st, dprobs, G, nprob, smem);
+        case 8: return solve_R<8>(st, dprobs, G, nprob, smem);
+        default: return solve_R<48>(st, dprobs, G, nprob, smem);
     }
 }
 
@@ -55,7 +56,8 @@ cudaError_t GS_CAT(gs_launch_cdpass_, GS_SUF)(int R, cudaStream_t st, const Solv
         case 1: return cdpass_R<1>(st, dprobs, smem);
         case 2: return cdpass_R<2>(st, dprobs, smem);
         case 4: return cdpass_R<4>(st, dprobs, smem);
-        default: return cdpass_R<8>(st, dprobs, smem);
+        case 8: return cdpass_R<8>(st, dprobs, smem);
+        default: return cdpass_R<48>(st, dprobs, smem);
     }
 }
 
@@ -65,7 +67,8 @@ cudaError_t GS_CAT(gs_launch_batch_, GS_SUF)(int R, cudaStream_t st, SolveDev* d
         case 1: return batch_R<1>(st, dprobs, douts, B, smem);
         case 2: return batch_R<2>(st, dprobs, douts, B, smem);
         case 4: return batch_R<4>(st, dprobs, douts, B, smem);
-        default: return batch_R<8>(st, dprobs, douts, B, smem);
+        case 8: return batch_R<8>(st, dprobs, douts, B, smem);
+        default: return cudaErrorInvalidValue;     // batched problems: n <= 1792
     }
 }
 

@@ -90,6 +90,29 @@ def cfg1(p=100_000, n=1000):
     return make_dense_case("cfg1", 1, n, p, 0.3, 100, "normal", 3.0, 100, 2.0, 1e-8)
 
 
+def cfg2(p=1_000_000, n=10_000, k=500, block=10_000):
+    """configs[2]: n x p i.i.d. N(0,1) float32 entries, generated per
+    10000-column block with ``default_rng([2, block])``, columns scaled to
+    unit norm with float64 norms and stored as float32; 500 +-1
+    coefficients; SNR 3 (unstated in BASELINE.json: recorded in ``meta``);
+    50 lambdas to lambda_max / 20; tolerance 1e-5.  The full size is a
+    40 GB design: tests use a column prefix (``p``), which is the same
+    generator's first blocks."""
+    X = np.empty((n, p), dtype=np.float32, order="F")
+    for b0 in range(0, p, block):
+        b1 = min(p, b0 + block)
+        Z = np.random.default_rng([2, b0 // block]).standard_normal((b1 - b0, n), dtype=np.float32)
+        Zd = Z.astype(np.float64)
+        Zd /= np.sqrt(np.einsum("ij,ij->i", Zd, Zd))[:, None]
+        X[:, b0:b1] = Zd.T.astype(np.float32)
+    rng = np.random.default_rng(2)
+    beta = _support(rng, p, min(k, p), "pm1")
+    y = _response(rng, X, beta, 3.0)
+    return LassoPathCase("cfg2", X, y, 50, float(np.log10(20.0)), 1e-5, beta,
+                         dict(n=n, p=p, k=min(k, p), values="pm1", snr=3.0, snr_note="unstated in BASELINE; 3 used",
+                              storage="dense-f32"))
+
+
 def cfg3(p=1_000_000, n=20_000, nnz_per_col=20):
     """configs[3]: CSC n x p, exactly ``nnz_per_col`` rows per column drawn
     uniformly without replacement, lognormal(0,1) values, unit column norms,
@@ -133,4 +156,4 @@ def cfg4_rows(b: int, n0: int = 1000, n: int = 500) -> np.ndarray:
 
 
 def by_name(name: str, **kw) -> LassoPathCase:
-    return {"cfg0": cfg0, "cfg1": cfg1, "cfg3": cfg3}[name](**kw)
+    return {"cfg0": cfg0, "cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3}[name](**kw)

@@ -245,3 +245,21 @@ def test_path_sparse_certify_identical():
     b = gs.run_path(Xd, y, grid, gs.SolverConfig(epsilon=eps, max_passes=100_000, certify=False), solver=dev)
     assert np.array_equal(a.betas, b.betas)
     assert [x.gap for x in a.certs] == [x.gap for x in b.certs]
+
+
+@pytest.mark.parametrize("n, p, T", [(2000, 1500, 10), (10_000, 3000, 12)])
+def test_path_cfg2_generator_long_columns(n, p, T):
+    """configs[2] generator (float32 storage, unit-norm N(0,1) columns, tol 1e-5,
+    grid to lambda_max / 20) at long column lengths: the 48-rows-per-lane CD
+    with columns streamed from the shared-memory ring, against the oracle on
+    the upcast values."""
+    c = synth.cfg2(p=p, n=n, k=min(500, p // 4))
+    X64 = np.asfortranarray(c.X.astype(np.float64))
+    X = gs.DesignMatrix(c.X)
+    Xo = O.DesignMatrix(X64)
+    lmax, _ = Xo.max_abs_correlation(c.y)
+    grid = O.lambda_grid(lmax, T, c.delta)
+    ra = gs.run_path(X, c.y, grid, gs.SolverConfig(epsilon=c.epsilon, max_passes=100_000))
+    rb = O.run_path(Xo, c.y, grid, O.SolverConfig(epsilon=c.epsilon, max_passes=100_000))
+    compare_paths(ra, rb, float(c.y @ c.y))
+    assert np.all(ra.converged)
