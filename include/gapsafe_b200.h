@@ -136,6 +136,11 @@ typedef struct {
  * (problem.py:50 recomputes it per LassoProblem; the value is identical). */
 int gs_solver_create(const gs_matrix *M, const double *y, gs_solver **out);
 int gs_solver_lambda_max(gs_solver *S, double *lambda_max, int64_t *j_star, double *y_norm_sq);
+/* Override lambda_max (LassoProblem(X, y, lam, lambda_max=...) of the oracle;
+ * problem.py:50): a solver over a gathered column subset X_A of a sharded
+ * design takes the full design's lambda_max, so the lambda >= lambda_max
+ * shortcut (solver.py:160-161) is decided on the whole problem. */
+int gs_solver_set_lambda_max(gs_solver *S, double lambda_max);
 /* warm start (solver.py:164-169): beta == NULL -> zeros */
 int gs_solver_set_beta(gs_solver *S, const double *beta);
 /* Sequential gap-sphere screen at lam from the previous solve's (beta, theta,

@@ -81,6 +81,7 @@ SIGNATURES = {
     "gs_vec_stats": (c_i32, [P_f64, P_f64, c_i64, P_f64, P_f64]),
     "gs_solver_create": (c_i32, [c_vp, P_f64, ctypes.POINTER(c_vp)]),
     "gs_solver_lambda_max": (c_i32, [c_vp, P_f64, P_i64, P_f64]),
+    "gs_solver_set_lambda_max": (c_i32, [c_vp, c_dbl]),
     "gs_solver_set_beta": (c_i32, [c_vp, P_f64]),
     "gs_solver_seq_screen": (c_i32, [c_vp, c_dbl, P_i64]),
     "gs_solver_solve": (c_i32, [c_vp, c_dbl, ctypes.POINTER(SolveConfig), P_i64, c_i64,

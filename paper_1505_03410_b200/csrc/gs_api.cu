@@ -678,6 +678,13 @@ extern "C" int gs_solver_create(const gs_matrix* M, const double* y, gs_solver**
     return GS_OK;
 }
 
+extern "C" int gs_solver_set_lambda_max(gs_solver* S, double lambda_max) {
+    if (!S) return fail(GS_ERR_VALUE, "null solver");
+    if (!(lambda_max > 0)) return fail(GS_ERR_VALUE, "lambda_max must be positive");
+    S->lmax = lambda_max;
+    return GS_OK;
+}
+
 extern "C" int gs_solver_lambda_max(gs_solver* S, double* lambda_max, int64_t* j_star, double* y_norm_sq) {
     if (lambda_max) *lambda_max = S->lmax;
     if (j_star) *j_star = S->jstar;

@@ -137,6 +137,12 @@ class DeviceSolver:
             self._lib.gs_solver_free(h)
             self._h = None
 
+    def set_lambda_max(self, lambda_max: float) -> None:
+        """Use the whole problem's lambda_max (sharded paths solve on a
+        gathered column subset; problem.py:50)."""
+        _lib.check(self._lib.gs_solver_set_lambda_max(self._h, float(lambda_max)))
+        self.lambda_max = float(lambda_max)
+
     def set_beta(self, beta):
         if beta is None:
             _lib.check(self._lib.gs_solver_set_beta(self._h, None))
