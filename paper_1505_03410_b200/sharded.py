@@ -215,3 +215,39 @@ def run_path_sharded(backend, y: np.ndarray, grid: np.ndarray, config: SolverCon
 def _nonzero_norms(backend) -> np.ndarray:
     norms = backend.X.col_norms if hasattr(backend, "X") else backend.col_norms
     return np.asarray(norms) > 0
+
+
+def run_batch_sharded(X0, y0: np.ndarray, rows: np.ndarray, grids: np.ndarray, config: SolverConfig):
+    """Independent problems sharded by problem index:
+    rank g runs problems ``shard_range(B, g, world)`` with one CTA each on its
+    own GPU (``BatchPathSolver``); X0 and y0 are replicated.  No collective on
+    the data path -- rank 0 gathers the per-problem (passes, gaps, converged,
+    n_active) at the end.  Returns the full (B, T) arrays on rank 0, None
+    elsewhere, plus the local device time (ms) on every rank."""
+    import torch
+    import torch.distributed as dist
+    from .solver import BatchPathSolver
+    rank, world = dist.get_rank(), dist.get_world_size()
+    B = rows.shape[0]
+    lo, hi = D.shard_range(B, rank, world)
+    T = grids.shape[1]
+    out = None
+    if hi > lo:
+        bs = BatchPathSolver(X0, y0, rows[lo:hi])
+        out = bs.run_paths(grids[lo:hi], config)
+    dev = D._device()
+    mx = max(D.shard_range(B, r, world)[1] - D.shard_range(B, r, world)[0] for r in range(world))
+    pack = torch.zeros((mx, T, 4), dtype=torch.float64, device=dev)
+    if out is not None:
+        loc = np.stack([out["passes"], out["gaps"], out["converged"], out["n_active"]], axis=-1).astype(np.float64)
+        pack[: hi - lo] = torch.as_tensor(loc)
+    parts = [torch.zeros_like(pack) for _ in range(world)] if rank == 0 else None
+    dist.gather(pack, parts, dst=0)
+    ms = out["device_ms"] if out is not None else 0.0
+    if rank != 0:
+        return None, ms
+    full = np.concatenate([parts[r][: D.shard_range(B, r, world)[1] - D.shard_range(B, r, world)[0]].cpu().numpy()
+                           for r in range(world)], axis=0)
+    res = dict(passes=full[..., 0].astype(np.int64), gaps=full[..., 1], converged=full[..., 2] > 0,
+               n_active=full[..., 3].astype(np.int64))
+    return res, ms

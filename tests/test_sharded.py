@@ -140,3 +140,54 @@ def test_sharded_path_gloo_oracle_backend():
 @pytest.mark.gpu
 def test_sharded_path_device_backend():
     _run(device=True)
+
+
+def _batch_worker(rank, world, port, q):
+    import torch.distributed as dist
+    import paper_1505_03410_b200 as gs
+    from paper_1505_03410_b200 import sharded, synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X0, y0, _ = synth.cfg4_shared(p=3000)
+        B = 6
+        rows = np.stack([synth.cfg4_rows(b) for b in range(B)]).astype(np.int32)
+        D0 = gs.DesignMatrix(X0)
+        lm = gs.BatchPathSolver(D0, y0, rows).lambda_max
+        grids = np.stack([gs.lambda_grid(lm[b], 8, 2.0) for b in range(B)])
+        cfg = gs.SolverConfig(epsilon=1e-8 * float(y0 @ y0) / 2, max_passes=100_000)
+        res, _ = sharded.run_batch_sharded(D0, y0, rows, grids, cfg)
+        if rank == 0:
+            single = gs.BatchPathSolver(D0, y0, rows).run_paths(grids, cfg)
+            q.put(("ok", (res, single)))
+        else:
+            q.put(("ok", None))
+    except Exception:
+        import traceback
+        q.put(("err", traceback.format_exc()))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_batch_problem_sharding_matches_single_process():
+    """cfg4 problem sharding: two ranks, three problems each, identical per-problem
+    epochs / gaps / active-set sizes to one process running all six."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+    errs = [o[1] for o in outs if o[0] == "err"]
+    assert not errs, errs[0]
+    res, single = next(o[1] for o in outs if o[1] is not None)
+    assert np.array_equal(res["passes"], single["passes"])
+    assert np.array_equal(res["n_active"], single["n_active"])
+    assert np.array_equal(res["converged"], single["converged"])
+    assert np.array_equal(res["gaps"], single["gaps"])
