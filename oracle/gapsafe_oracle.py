@@ -15,8 +15,9 @@ reference imported) and ``tests/test_oracle_golden.py`` pins this module to
 them.  Parity pin status: pinned (golden vectors + direct comparison with
 the reference where it is importable).
 
-Scope: the north_star path only -- rules ``none`` and ``gap_sphere``; the
-dome/static/dynamic/ST3 rules, Elastic-Net and I/O are out of scope
+Scope: the north_star path with every screening rule of the reference
+(``none``, ``static``, ``dynamic``, ``st3``, ``gap_sphere``, ``gap_dome``;
+regions.py:23-273, solver.py:104-126); Elastic-Net and I/O are out of scope
 (SURVEY.md §2).
 """
 
@@ -152,6 +153,14 @@ class DesignMatrix:
             v[self._mat.indices[lo:hi]] += a * self._mat.data[lo:hi]
         else:
             v[: self.n_base] += a * self._mat[:, j]
+
+    def col_dot(self, j, v):
+        """design_matrix.py:100-113 (no implicit tail in the oracle)."""
+        v = np.asarray(v, dtype=np.float64)
+        if self.is_sparse:
+            lo, hi = self._mat.indptr[j], self._mat.indptr[j + 1]
+            return float(np.dot(self._mat.data[lo:hi], v[self._mat.indices[lo:hi]]))
+        return float(np.dot(self._mat[:, j], v[: self.n_base]))
 
     def matvec(self, beta):
         """design_matrix.py:130-137."""
@@ -304,17 +313,47 @@ class Sphere:
 
 
 @dataclass(frozen=True)
+class Dome:
+    """regions.py:35-57: B(c, r) & {theta : n^T theta <= n^T c - ratio r}."""
+    center: np.ndarray
+    radius: float
+    ratio: float
+    normal: np.ndarray
+
+
+@dataclass(frozen=True)
 class ScreenResult:
     zero_set: np.ndarray
     active_set: np.ndarray
     mu: np.ndarray
 
 
-def mu_values(s, X, cols=None):
-    """regions.py:75-79 / 100-107 (sphere)."""
+def _sphere_mu_values(s, X, cols):
+    """regions.py:75-79."""
     ct = X.transpose_dot(s.center, cols=cols)
     norms = X.col_norms if cols is None else X.col_norms[cols]
     return np.abs(ct) + s.radius * norms
+
+
+def _dome_mu_values(d, X, cols):
+    """regions.py:82-97."""
+    ct = X.transpose_dot(d.center, cols=cols)
+    nt = X.transpose_dot(d.normal, cols=cols)
+    norms = X.col_norms if cols is None else X.col_norms[cols]
+    r, a = d.radius, min(max(d.ratio, -1.0), 1.0)
+    cross = r * np.sqrt(np.maximum(norms ** 2 - nt ** 2, 0.0) * (1.0 - a ** 2))
+    sig_pos = np.where(nt < -a * norms, ct + r * norms, ct - r * a * nt + cross)
+    sig_neg = np.where(-nt < -a * norms, -ct + r * norms, -ct + r * a * nt + cross)
+    return np.maximum(sig_pos, sig_neg)
+
+
+def mu_values(region, X, cols=None):
+    """regions.py:100-107."""
+    if isinstance(region, Sphere):
+        return _sphere_mu_values(region, X, cols)
+    if isinstance(region, Dome):
+        return _dome_mu_values(region, X, cols)
+    raise TypeError(f"unknown region type: {type(region)!r}")
 
 
 def screen(region, X, tol=SCREEN_SAFETY, cols=None):
@@ -340,8 +379,91 @@ def region_gap_sphere(prob, beta, theta, residual=None, gap=None):
                   radius=gap_radius(prob, gap))
 
 
+def region_static(prob):
+    """regions.py:162-165."""
+    r = abs(1.0 / prob.lam - 1.0 / prob.lambda_max) * np.sqrt(prob.y_norm_sq)
+    return Sphere(center=prob.y / prob.lam, radius=float(r))
+
+
+def region_dynamic(prob, theta):
+    """regions.py:168-174."""
+    if theta.feasibility_margin < -1e-9:
+        raise ValueError("theta must be dual feasible")
+    center = prob.y / prob.lam
+    return Sphere(center=center, radius=float(np.linalg.norm(theta.theta - center)))
+
+
+def region_st3(prob, theta):
+    """regions.py:177-197."""
+    if theta.feasibility_margin < -1e-9:
+        raise ValueError("theta must be dual feasible")
+    center = prob.y / prob.lam
+    big_r = float(np.linalg.norm(theta.theta - center))
+    xj = np.zeros(prob.X.n_cols)
+    xj[prob.j_star] = 1.0
+    col = prob.X.matvec(xj)
+    sgn = np.sign(prob.X.col_dot(prob.j_star, prob.y)) or 1.0
+    norm_j = prob.X.col_norms[prob.j_star]
+    dist = (prob.lambda_max / prob.lam - 1.0) / norm_j
+    radicand = big_r ** 2 - dist ** 2
+    if radicand < 0:
+        radicand = 0.0
+    new_center = center - (dist / norm_j) * sgn * col
+    return Sphere(center=new_center, radius=float(np.sqrt(radicand)))
+
+
+def inner_radius(prob, beta, residual=None):
+    """regions.py:235-247."""
+    beta = np.asarray(beta, dtype=np.float64)
+    if residual is None:
+        residual = prob.y - prob.X.matvec(beta)
+    val = prob.y_norm_sq - float(np.dot(residual, residual)) - 2.0 * prob.lam * float(np.sum(np.abs(beta)))
+    return float(np.sqrt(max(val, 0.0))) / prob.lam
+
+
+def region_gap_dome(prob, beta, theta, residual=None):
+    """regions.py:250-273."""
+    if theta.feasibility_margin < -1e-9:
+        raise ValueError("theta must be dual feasible")
+    yl = prob.y / prob.lam
+    diff = yl - theta.theta
+    big_r = float(np.linalg.norm(diff))
+    if big_r == 0.0:
+        return Sphere(center=np.array(theta.theta), radius=0.0)
+    r_in = inner_radius(prob, beta, residual=residual)
+    if r_in > big_r * (1 + 1e-9) + 1e-12:
+        raise NumericalInconsistencyError(f"inner radius {r_in} exceeds outer radius {big_r}")
+    r_in = min(r_in, big_r)
+    ratio = 2.0 * (r_in / big_r) ** 2 - 1.0
+    return Dome(center=0.5 * (yl + theta.theta), radius=0.5 * big_r, ratio=ratio, normal=diff / big_r)
+
+
+def _make_region(rule, prob, beta, theta, rho, gap):
+    """solver.py:104-119."""
+    if rule == "none":
+        return None
+    if rule == "static":
+        return region_static(prob)
+    if rule == "dynamic":
+        return region_dynamic(prob, theta)
+    if rule == "st3":
+        return region_st3(prob, theta)
+    if rule == "gap_sphere":
+        return region_gap_sphere(prob, beta, theta, gap=gap)
+    if rule == "gap_dome":
+        return region_gap_dome(prob, beta, theta, residual=rho)
+    raise ValueError(f"unknown rule {rule}")
+
+
+def _trace_radius(rule, region, prob, gap):
+    """solver.py:122-126."""
+    if rule in ("none", "gap_sphere", "gap_dome"):
+        return gap_radius(prob, max(gap, 0.0))
+    return region.radius if region is not None else float("nan")
+
+
 # ---------------------------------------------------------------------------
-# solver.py (rules none / gap_sphere)
+# solver.py
 # ---------------------------------------------------------------------------
 
 @dataclass
@@ -355,8 +477,8 @@ class SolverConfig:
 
     def __post_init__(self):
         self.rule = getattr(self.rule, "value", self.rule)
-        if self.rule not in ("none", "gap_sphere"):
-            raise ValueError(f"oracle supports rules none/gap_sphere, not {self.rule}")
+        if self.rule not in ("none", "static", "dynamic", "st3", "gap_sphere", "gap_dome"):
+            raise ValueError(f"unknown rule {self.rule}")
 
 
 @dataclass
@@ -429,8 +551,8 @@ def solve(prob, config, warm_beta=None, active0=None):
                 break
             theta = dual_scale(prob, rho, restrict=state.active)
             pre_gap = duality_gap(prob, beta, theta, residual=rho).gap
-            if config.rule == "gap_sphere":
-                region = region_gap_sphere(prob, beta, theta, gap=pre_gap)
+            region = _make_region(config.rule, prob, beta, theta, rho, pre_gap)
+            if region is not None:
                 mus = mu_values(region, X, cols=state.active)
                 keep = mus >= 1.0 - SCREEN_SAFETY
                 dropped = state.active[~keep]
@@ -443,7 +565,7 @@ def solve(prob, config, warm_beta=None, active0=None):
             cert = duality_gap(prob, beta, theta, residual=rho)
             state.theta, state.cert = theta, cert
             state.screen_trace.append((state.passes_done, state.active.size, cert.gap,
-                                       gap_radius(prob, max(cert.gap, 0.0))))
+                                       _trace_radius(config.rule, region, prob, cert.gap)))
             if config.track_active:
                 state.active_history.append(state.active.copy())
             if config.on_checkpoint is not None:
@@ -512,8 +634,11 @@ def run_path(X, y, grid, config, cache_lambda_max=False, max_points=None, time_b
         warm = None if prev_beta is None else prev_beta
         active0 = None
         if (prev_theta is not None and not prev_theta.interpolating
-                and config.rule == "gap_sphere"):
-            region = region_gap_sphere(prob, prev_beta, prev_theta, residual=prev_resid)
+                and config.rule in ("gap_sphere", "gap_dome")):
+            if config.rule == "gap_sphere":
+                region = region_gap_sphere(prob, prev_beta, prev_theta, residual=prev_resid)
+            else:
+                region = region_gap_dome(prob, prev_beta, prev_theta, residual=prev_resid)
             active0 = screen(region, X).active_set
         beta, cert, state = solve(prob, config, warm_beta=warm, active0=active0)
         timings.append(time.perf_counter() - t0)

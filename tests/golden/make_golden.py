@@ -67,6 +67,48 @@ def path_cases():
     }
 
 
+RULES = ("static", "dynamic", "st3", "gap_dome")
+
+
+def rule_cases():
+    """Every non-default screening rule on a dense and a CSC case."""
+    sys.path.insert(0, ROOT)
+    from paper_1505_03410_b200 import synth
+    c0 = synth.cfg0(p=500)
+    c3 = synth.cfg3(p=2000, n=300, nnz_per_col=10)
+    return {
+        "rules_cfg0_p500": (c0.X, c0.y, 8, 2.0, c0.epsilon),
+        "rules_cfg3_n300_p2000": (c3.X, c3.y, 8, 2.0, c3.epsilon),
+    }
+
+
+def _record(res, eps):
+    traces = [np.array(t, dtype=np.float64).reshape(-1, 4) for t in res.traces]
+    return dict(betas=res.betas, epsilon=np.float64(eps),
+                passes=np.array([s.passes_done for s in res.states]),
+                gaps=np.array([c.gap for c in res.certs]),
+                converged=res.converged,
+                trace_rows=np.array([t.shape[0] for t in traces]),
+                traces=np.concatenate(traces),
+                active_sizes=np.array([s.active.size for s in res.states]),
+                actives=np.concatenate([s.active for s in res.states]))
+
+
+def main_rules():
+    G = _import_reference()
+    for name, (Xh, y, T, delta, eps) in rule_cases().items():
+        D = G.DesignMatrix(Xh)
+        lmax, _ = D.max_abs_correlation(y)
+        grid = G.lambda_grid(lmax, T, delta)
+        rec = {"grid": grid}
+        for rule in RULES:
+            res = G.run_path(D, y, grid, G.SolverConfig(epsilon=eps, max_passes=100_000, rule=G.Rule(rule)))
+            for k2, v2 in _record(res, eps).items():
+                rec[f"{rule}__{k2}"] = v2
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), **rec)
+        print(name, {r: int(rec[f"{r}__passes"].sum()) for r in RULES})
+
+
 def main():
     G = _import_reference()
     from gapsafe import _kernels as K
@@ -112,4 +154,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "rules":
+        main_rules()
+    else:
+        main()
+        main_rules()

@@ -60,6 +60,27 @@ def test_oracle_path_matches_reference_golden(name):
     assert np.array_equal(np.stack([s.theta.theta for s in res.states]), g["thetas"])
 
 
+@pytest.mark.parametrize("name", ["rules_cfg0_p500", "rules_cfg3_n300_p2000"])
+def test_oracle_rules_match_reference_golden(name):
+    """static / dynamic / st3 / gap_dome (regions.py:159-273, solver.py:104-126):
+    the oracle reproduces the reference's paths bit for bit."""
+    from make_golden import RULES, rule_cases
+    Xh, y, T, delta, eps = rule_cases()[name]
+    g = np.load(os.path.join(GOLD, name + ".npz"))
+    X = O.DesignMatrix(Xh)
+    lmax, _ = X.max_abs_correlation(y)
+    grid = O.lambda_grid(lmax, T, delta)
+    assert np.array_equal(grid, g["grid"])
+    for rule in RULES:
+        res = O.run_path(X, y, grid, O.SolverConfig(epsilon=eps, max_passes=100_000, rule=rule))
+        assert np.array_equal(np.array([s.passes_done for s in res.states]), g[f"{rule}__passes"]), rule
+        assert np.array_equal(res.betas, g[f"{rule}__betas"]), rule
+        assert np.array_equal(np.array([c.gap for c in res.certs]), g[f"{rule}__gaps"]), rule
+        traces = np.concatenate([np.array(t, dtype=np.float64).reshape(-1, 4) for t in res.traces])
+        assert np.array_equal(traces, g[f"{rule}__traces"]), rule
+        assert np.array_equal(np.concatenate([s.active for s in res.states]), g[f"{rule}__actives"]), rule
+
+
 def _diag(lam=1.0):
     return O.LassoProblem(O.DesignMatrix(np.array([[1.0, 0.0], [0.0, 2.0]])), np.array([1.0, 1.0]), lam)
 
