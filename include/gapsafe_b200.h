@@ -38,6 +38,10 @@ extern "C" {
 
 #define GS_RULE_NONE 0          /* solver.py:27 Rule.NONE       */
 #define GS_RULE_GAP_SPHERE 1    /* solver.py:31 Rule.GAP_SPHERE */
+#define GS_RULE_STATIC 2        /* solver.py:28 Rule.STATIC, regions.py:162-165  */
+#define GS_RULE_DYNAMIC 3       /* solver.py:29 Rule.DYNAMIC, regions.py:168-174 */
+#define GS_RULE_ST3 4           /* solver.py:30 Rule.ST3, regions.py:177-197     */
+#define GS_RULE_GAP_DOME 5      /* solver.py:32 Rule.GAP_DOME, regions.py:235-273 */
 
 typedef struct gs_matrix gs_matrix;
 typedef struct gs_solver gs_solver;

@@ -27,6 +27,10 @@ GS_DTYPE_F64 = 0
 GS_DTYPE_F32 = 1
 GS_RULE_NONE = 0
 GS_RULE_GAP_SPHERE = 1
+GS_RULE_STATIC = 2
+GS_RULE_DYNAMIC = 3
+GS_RULE_ST3 = 4
+GS_RULE_GAP_DOME = 5
 
 c_i64 = ctypes.c_int64
 c_i32 = ctypes.c_int32

@@ -568,6 +568,9 @@ struct gs_solver {
     int G = 1;
     double lmax = 0.0, y_norm_sq = 0.0;
     int64_t jstar = 0;
+    double* q = nullptr;          // X^T y (static / dynamic / ST3 / dome centres)
+    double* gstar = nullptr;      // X^T x_jstar (ST3), built on first use
+    bool gstar_ready = false;
     int64_t m = 0;                // active count after the last solve
     bool has_prev = false, seq_pending = false;
     double seq_lam = 0.0;
@@ -585,6 +588,7 @@ static void solver_release(gs_solver* S) {
     cudaFree(S->flags); cudaFree(S->mark); cudaFree(S->partial);
     cudaFree(S->sc); cudaFreeHost(S->hs); cudaFree(S->ctl); cudaFreeHost(S->hctl); cudaFree(S->bar);
     cudaFree(S->cta_val); cudaFree(S->cta_idx); cudaFree(S->cta_cnt); cudaFree(S->dprob); cudaFree(S->trace);
+    cudaFree(S->q); cudaFree(S->gstar);
     S->s.release();
     if (S->ev0) cudaEventDestroy(S->ev0);
     if (S->ev1) cudaEventDestroy(S->ev1);
@@ -654,8 +658,10 @@ extern "C" int gs_solver_create(const gs_matrix* M, const double* y, gs_solver**
         CK(cudaMemcpyAsync(S->y, y, n * 8, cudaMemcpyHostToDevice, S->st));
         TRY(sc_upload(S));
         // lambda_max = |X^T y|_inf, j_star (problem.py:50), ||y||^2 (problem.py:54)
+        TRY(dalloc(&S->q, p));
         GemvArgs a{};
         a.v = S->y; a.m = p; a.mode = GEMV_MAX; a.blk_val = S->s.blk_val; a.blk_idx = S->s.blk_idx;
+        a.out_c = S->q;                    // X^T y kept for the static/dynamic/ST3/dome centres
         int64_t nb = 0;
         TRY(launch_gemv(M, S->st, a, &nb));
         k_max_finalize<<<1, 1024, 0, S->st>>>(S->s.blk_val, S->s.blk_idx, nb, &S->sc->corr, &S->sc->corr_arg);
@@ -708,9 +714,10 @@ static int status_error(int32_t st, double margin, double gap) {
         return fail(GS_ERR_INFEASIBLE, buf);
     }
     if (st == ST_NEG_GAP) {
-        snprintf(buf, sizeof buf, "negative duality gap beyond tolerance: %.17g", gap);
+        snprintf(buf, sizeof buf, "negative duality gap / inner radius beyond tolerance: %.17g", gap);
         return fail(GS_ERR_NUMERICAL, buf);
     }
+    if (st == ST_VALUE) return fail(GS_ERR_VALUE, "theta must be dual feasible");
     return GS_OK;
 }
 
@@ -785,6 +792,46 @@ static void fill_dev(gs_solver* S, SolveDev& d) {
     d.cd_gram = eg ? atoi(eg) : cd_gram_default(M->n);
     const char* ep = getenv("GS_CD_PROF");
     d.cd_prof = ep ? atoi(ep) : 0;
+    d.q = S->q; d.gstar = S->gstar; d.lmax_path = S->lmax; d.jstar = S->jstar;
+}
+
+// column j of the design as a dense f64 n-vector (regions.py:187: X.matvec(e_j))
+static __global__ void k_densify_col(const void* X, int dtype, int64_t ld, const double* data, const int32_t* indices,
+                                     const int64_t* indptr, int sparse, int64_t j, int n, double* out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sparse) {          // out was zeroed by the caller
+        if (blockIdx.x == 0)
+            for (int64_t q = indptr[j] + threadIdx.x; q < indptr[j + 1]; q += blockDim.x) out[indices[q]] = data[q];
+    } else if (r < n) {
+        out[r] = dtype == GS_DTYPE_F64 ? ((const double*)X)[j * ld + r] : (double)((const float*)X)[j * ld + r];
+    }
+}
+
+// gstar = X^T x_jstar for the ST3 centre (regions.py:186-196), once per solver
+static int ensure_gstar(gs_solver* S) {
+    if (S->gstar_ready) return GS_OK;
+    const gs_matrix* M = S->M;
+    cudaStream_t st = S->st;
+    if (!S->gstar) TRY(dalloc(&S->gstar, S->p));
+    double* col;
+    TRY(dalloc(&col, S->n + 2));
+    CK(cudaMemsetAsync(col, 0, (S->n + 2) * 8, st));
+    const int blocks = M->sparse ? 1 : (int)((S->n + 255) / 256);
+    if (M->sparse && S->n > 0) {
+        // one block: zero then scatter (single-block kernel keeps the order)
+        k_densify_col<<<1, 1024, 0, st>>>(nullptr, 0, 0, M->data, M->indices, M->indptr, 1, S->jstar, 0, col);
+    } else {
+        k_densify_col<<<blocks, 256, 0, st>>>(M->X, M->dtype, M->ld, nullptr, nullptr, nullptr, 0, S->jstar,
+                                              (int)S->n, col);
+    }
+    CKL();
+    GemvArgs a{};
+    a.v = col; a.m = S->p; a.mode = GEMV_RAW; a.out_c = S->gstar;
+    TRY(launch_gemv(M, st, a, nullptr));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(col);
+    S->gstar_ready = true;
+    return GS_OK;
 }
 
 extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* cfg, const int64_t* active0,
@@ -793,13 +840,17 @@ extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* 
     if (cfg->epsilon <= 0) return fail(GS_ERR_VALUE, "epsilon must be positive");
     if (cfg->screen_every < 1) return fail(GS_ERR_VALUE, "screen_every must be at least 1");
     if (cfg->max_passes < 1) return fail(GS_ERR_VALUE, "max_passes must be at least 1");
+    if (cfg->rule < GS_RULE_NONE || cfg->rule > GS_RULE_GAP_DOME) return fail(GS_ERR_VALUE, "unknown rule");
     if (active0_mode == 2 && !(S->seq_pending && S->seq_lam == lam))
         return fail(GS_ERR_VALUE, "active0_mode 2 needs gs_solver_seq_screen at the same lambda");
+    if (active0_mode == 2 && cfg->rule != GS_RULE_GAP_SPHERE && cfg->rule != GS_RULE_GAP_DOME)
+        return fail(GS_ERR_VALUE, "the sequential screen is defined for the gap sphere and gap dome rules");
     S->seq_pending = false;
     const gs_matrix* M = S->M;
     cudaStream_t st = S->st;
+    if (cfg->rule == GS_RULE_ST3) TRY(ensure_gstar(S));
     const int64_t p = S->p;
-    const bool gap_rule = cfg->rule == GS_RULE_GAP_SPHERE;
+    const bool screening = cfg->rule != GS_RULE_NONE;
     const int64_t f = cfg->screen_every;
     TRY(ensure_trace(S, cfg->max_passes / f + 4));
     DevScalars* h = S->hs;
@@ -817,7 +868,7 @@ extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* 
         CK(cudaMemcpyAsync(S->rho, S->y, S->n * 8, cudaMemcpyDeviceToDevice, st));
         k_scale_vec<<<grid_for(S->n, 256), 256, 0, st>>>(S->y, lam, S->n, S->theta, 1);
         CKL();
-        if (gap_rule) {
+        if (screening) {
             GemvArgs a{};
             a.v = S->theta; a.m = p; a.mode = GEMV_MU; a.scale = 1.0; a.radius_host = 0.0;
             a.thresh = 1.0 - 1e-9; a.norms = M->norms; a.flags = S->flags;
@@ -1252,6 +1303,8 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
     if (cfg->epsilon <= 0) return fail(GS_ERR_VALUE, "epsilon must be positive");
     if (cfg->screen_every < 1 || cfg->max_passes < 1) return fail(GS_ERR_VALUE, "bad solver configuration");
     if (cfg->on_checkpoint) return fail(GS_ERR_VALUE, "checkpoint hooks are not available in batched mode");
+    if (cfg->rule != GS_RULE_NONE && cfg->rule != GS_RULE_GAP_SPHERE)
+        return fail(GS_ERR_VALUE, "batched problems run the none / gap_sphere rules");
     const int64_t B = Bt->B, p = Bt->p, n = Bt->n, ld = Bt->ld;
     cudaStream_t st = Bt->st;
     const size_t es = Bt->dtype == GS_DTYPE_F64 ? 8 : 4;

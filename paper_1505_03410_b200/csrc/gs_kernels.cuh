@@ -30,6 +30,11 @@ struct DevScalars {
     double l1, primal, dual, gap_pre, radius, primal_post, gap_post, radius_post;
     // certification anchor
     double rho_norm_ub;
+    // screening-rule region (regions.py:159-273): |theta - y/lam|^2, radius,
+    // ST3 centre coefficient, dome outer radius R, ball radius R/2, cut ratio;
+    // trace radius for the rules whose trace reports the region radius
+    double dsq, rule_r, rule_coef, rule_R, rule_rd, rule_a, rule_trace_r;
+    int32_t rule_trace_fixed, rule_pad;
     // counts
     int64_t m;            // active-set size
     int64_t cnt;          // generic compaction output count
@@ -44,8 +49,24 @@ struct TraceRow { int64_t passes, n_active; double gap, radius; };
 enum Status : int32_t {
     ST_OK = 0,
     ST_INFEASIBLE = 1,     // InfeasibleDualError   (problem.py:74-76)
-    ST_NEG_GAP = 2,        // NumericalInconsistencyError (regions.py:215-217)
+    ST_NEG_GAP = 2,        // NumericalInconsistencyError (regions.py:215-217, 266-268)
+    ST_VALUE = 3,          // ValueError: dome/dynamic/ST3 centre infeasible (regions.py:170, 183, 258)
 };
+
+enum RuleId : int32_t { R_NONE = 0, R_GAP_SPHERE = 1, R_STATIC = 2, R_DYNAMIC = 3, R_ST3 = 4, R_GAP_DOME = 5 };
+
+// Dome support test (regions.py:82-97) for the gap dome of regions.py:250-273:
+// qy = x^T y / lam, th = x^T theta, centre (y/lam + theta)/2, unit normal
+// (y/lam - theta)/R, ball radius r = R/2, clamped cut ratio a.
+__device__ __forceinline__ double dome_mu(double qy, double th, double R, double r, double a, double nrm) {
+    if (R == 0.0) return fabs(th);                       // Sphere(theta, 0)
+    const double ct = 0.5 * qy + 0.5 * th;
+    const double nt = (qy - th) / R;
+    const double cross = r * sqrt(fmax(nrm * nrm - nt * nt, 0.0) * (1.0 - a * a));
+    const double sp = (nt < -a * nrm) ? ct + r * nrm : ct - r * a * nt + cross;
+    const double sn = (-nt < -a * nrm) ? -ct + r * nrm : -ct + r * a * nt + cross;
+    return fmax(sp, sn);
+}
 
 // ---------------------------------------------------------------------------
 // column dot products (warp per column), fixed order, FMA

@@ -112,6 +112,11 @@ struct SolveDev {
     int cd_bytes;        // dense CD shared-memory region (tile + ring), GEMV staging after it
     int vs_cap;          // max n staged in shared memory for the GEMV
     int cd_gram;         // dense CD: Gram-window consumer (1) or one reduction per coordinate (0)
+    // screening rules other than the gap sphere: q = X^T y, gstar = X^T x_jstar (ST3)
+    const double* q;
+    const double* gstar;
+    double lmax_path;
+    int64_t jstar;
     int cd_prof;         // print Gram-window phase cycles at the end of each solve (debug)
 };
 
@@ -288,7 +293,9 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
     // per-column epilogue (lane 0); nrm/bj were loaded before the dot
     auto epilogue = [&](int64_t i, int64_t j, double cval, double nrm, double bj) {
         if (mode == G_MU) {
-            const double mu = fabs(cval) + radius * nrm;
+            const double mu = (P.rule == R_GAP_DOME && P.q)
+                                  ? dome_mu(__ldg(P.q + j) / P.lam, cval, P.sc->rule_R, P.sc->rule_rd, P.sc->rule_a, nrm)
+                                  : fabs(cval) + radius * nrm;
             P.mark[j] = (mu >= 1.0 - 1e-9) && nrm > 0.0;
         } else {
             if (out_c) out_c[i] = cval;
@@ -540,7 +547,7 @@ static __device__ void cta_dual(const SolveDev& P, double corr, int want_radius,
         const double primal = 0.5 * rho_sq + lam * l1s;
         const double gap = primal - dual;
         sc->rho_sq = rho_sq; sc->y_rho = y_rho; sc->alpha = alpha; sc->margin = margin; sc->interp = interp;
-        sc->corr = corr; sc->l1 = l1s; sc->primal = primal; sc->dual = dual; sc->gap_pre = gap;
+        sc->corr = corr; sc->l1 = l1s; sc->primal = primal; sc->dual = dual; sc->gap_pre = gap; sc->dsq = dsq;
         int st = ST_OK;
         if (margin < -1e-9) st = ST_INFEASIBLE;
         else if (want_radius && gap < -1e-10) st = ST_NEG_GAP;
@@ -549,6 +556,66 @@ static __device__ void cta_dual(const SolveDev& P, double corr, int want_radius,
         sc->rho_norm_ub = __dsqrt_ru(rho_sq_ru);
     }
     __syncthreads();
+}
+
+// mu_C(x_j) of the checkpoint region (regions.py:75-97) from the restricted dot
+// c = x_j^T rho (theta = alpha rho) and q_j = x_j^T y (solver.py:104-119)
+static __device__ __forceinline__ double rule_mu(const SolveDev& P, const DevScalars* sc, double c, int32_t j,
+                                                 double nrm) {
+    switch (P.rule) {
+        case R_STATIC:
+        case R_DYNAMIC: return fabs(__ldg(P.q + j) / P.lam) + sc->rule_r * nrm;
+        case R_ST3: return fabs(__ldg(P.q + j) / P.lam - sc->rule_coef * __ldg(P.gstar + j)) + sc->rule_r * nrm;
+        case R_GAP_DOME: return dome_mu(__ldg(P.q + j) / P.lam, sc->alpha * c, sc->rule_R, sc->rule_rd, sc->rule_a, nrm);
+        default: return fabs(sc->alpha * c) + sc->radius * nrm;
+    }
+}
+
+// region scalars of the checkpoint (thread 0 of CTA 0, after cta_dual):
+// regions.py:162-165 (static), 168-174 (dynamic), 177-197 (ST3), 235-273 (dome)
+static __device__ void rule_scalars(const SolveDev& P, DevScalars* sc) {
+    const double lam = P.lam;
+    sc->rule_trace_fixed = 0;
+    if (sc->status != ST_OK) return;
+    switch (P.rule) {
+        case R_STATIC: {
+            const double r = fabs(1.0 / lam - 1.0 / P.lmax_path) * sqrt(sc->y_norm_sq);
+            sc->rule_r = r; sc->rule_trace_r = r; sc->rule_trace_fixed = 1;
+            break;
+        }
+        case R_DYNAMIC: {
+            const double r = sqrt(sc->dsq);
+            sc->rule_r = r; sc->rule_trace_r = r; sc->rule_trace_fixed = 1;
+            break;
+        }
+        case R_ST3: {
+            const double big_r = sqrt(sc->dsq);
+            const double nrm = __ldg(P.norms + P.jstar);
+            const double qs = __ldg(P.q + P.jstar);
+            const double sgn = qs > 0.0 ? 1.0 : (qs < 0.0 ? -1.0 : 1.0);
+            const double dist = (P.lmax_path / lam - 1.0) / nrm;
+            double rad = big_r * big_r - dist * dist;
+            if (rad < 0.0) rad = 0.0;
+            sc->rule_coef = (dist / nrm) * sgn;
+            sc->rule_r = sqrt(rad); sc->rule_trace_r = sc->rule_r; sc->rule_trace_fixed = 1;
+            break;
+        }
+        case R_GAP_DOME: {
+            const double big_r = sqrt(sc->dsq);
+            sc->rule_R = big_r;
+            if (big_r > 0.0) {
+                const double val = sc->y_norm_sq - sc->rho_sq - 2.0 * lam * sc->l1;
+                double r_in = sqrt(fmax(val, 0.0)) / lam;
+                if (r_in > big_r * (1 + 1e-9) + 1e-12) { sc->status = ST_NEG_GAP; return; }
+                r_in = fmin(r_in, big_r);
+                const double ratio = 2.0 * (r_in / big_r) * (r_in / big_r) - 1.0;
+                sc->rule_rd = 0.5 * big_r;
+                sc->rule_a = fmin(fmax(ratio, -1.0), 1.0);
+            }
+            break;
+        }
+        default: break;
+    }
 }
 
 // post-drop certificate (solver.py:217-221): zero the dropped beta, add the
@@ -592,7 +659,9 @@ static __device__ void cta_post(const SolveDev& P, double* red) {
                                   __dmul_ru(2.3e-16 * (double)imax64(nd, 1), __dadd_ru(anchor, drift)));
         if (nd == 0) ctl->cd_delta = 0.0;
         sc->rho_norm_ub = __dsqrt_ru(rho_sq_ru);
-        if (ctl->ntrace < P.trace_cap) P.trace[ctl->ntrace] = TraceRow{ctl->passes, sc->m, gap, sc->radius_post};
+        // solver.py:122-126: region radius for static/dynamic/ST3, gap radius otherwise
+        const double tr = sc->rule_trace_fixed ? sc->rule_trace_r : sc->radius_post;
+        if (ctl->ntrace < P.trace_cap) P.trace[ctl->ntrace] = TraceRow{ctl->passes, sc->m, gap, tr};
         ctl->ntrace++;
     }
     __syncthreads();
@@ -1272,26 +1341,44 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
         const int cmask = min(7, (K >> 2) - 1);     // consumed is signalled every cmask+1 entries
         const unsigned mycons_s = cons_s + 4u * w;
         bool gram = false;
-        if constexpr (R <= 8) gram = P.cd_gram != 0;     // member rows held in registers: R <= 8 only
+        if constexpr (R <= 4) gram = P.cd_gram != 0;     // member rows held in registers: R <= 4 only
         if (gram) {
-            if constexpr (R <= 8)
+            if constexpr (R <= 4)
                 cd_consume_gram<T, R>(P, m, W, ring, sbytes, kmask, bar_s, kshift, cons_s, fin_s, reqg_s, reqp_s, dpub_s, cc,
                                       gw, ts, use_t, rho0, rr, D, gstep, n_unc, n_nz, n_req, n_cand, n_skip, tid);
-        } else
+        } else {
+        bool pf = false;                 // entry k was prefetched under entry k-1's reduction
+        int pf_pos = 0, pf_hg = 0, pf_j = 0;
+        double pf_tc = 0.0, pf_dp = 0.0, pf_bj = 0.0, pf_ns = 0.0, pf_iv = 0.0, pf_uq = 0.0, pf_nr = 0.0;
+        constexpr int RN = R <= 8 ? R : 1;
+        double xvn[RN];
+#pragma unroll
+        for (int q = 0; q < RN; ++q) xvn[q] = 0.0;
         for (int k = 0;; ++k) {
             const int s = k & kmask;
             // entries before k are fully read: consumed is signalled in batches (release store)
             if (k > 0 && (k & cmask) == 0) { __syncwarp(); if (lane == 0) st_rel_s(mycons_s, k); }
-            // one poll per entry: header and bytes are published together through the slot mbarrier
-            const unsigned par = (unsigned)((k >> kshift) & 1);
-            if (!mbar_test_s(bar_s + 8u * s, par)) {
-                const unsigned long long t0 = gtimer();
-                while (!mbar_test_s(bar_s + 8u * s, par)) spin_guard(t0, 4, k, gen, last, 0);
+            // one poll per entry (unless it was prefetched under the previous
+            // entry's reduction): header and bytes are published together
+            // through the slot mbarrier
+            int pos, hg, j;
+            double tc, dp, bj, ns, iv, uq, nr;
+            if (pf) {
+                pos = pf_pos; hg = pf_hg; j = pf_j; tc = pf_tc; dp = pf_dp;
+                bj = pf_bj; ns = pf_ns; iv = pf_iv; uq = pf_uq; nr = pf_nr;
+            } else {
+                const unsigned par = (unsigned)((k >> kshift) & 1);
+                if (!mbar_test_s(bar_s + 8u * s, par)) {
+                    const unsigned long long t0 = gtimer();
+                    while (!mbar_test_s(bar_s + 8u * s, par)) spin_guard(t0, 4, k, gen, last, 0);
+                }
+                const SlotHdr* h0 = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
+                pos = h0->pos; hg = h0->gen; j = h0->j; tc = h0->tcert; dp = h0->dp;
+                bj = h0->ci.beta; ns = h0->ci.ns; iv = h0->ci.inv; uq = h0->ci.u; nr = h0->ci.nr;
             }
+            const bool had_pf = pf;
+            pf = false;
             const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
-            const int pos = h->pos;
-            const int hg = h->gen;
-            const double tc = h->tcert, dp = h->dp;
             bool process = hg == gen && pos < m;
             if (hg == gen && use_t && D > dp) {
                 // drift outgrew the queue's bound (for the end entry: the positions
@@ -1314,8 +1401,6 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 continue;
             }
             ++n_cand;
-            const double bj = h->ci.beta, ns = h->ci.ns, iv = h->ci.inv, uq = h->ci.u, nr = h->ci.nr;
-            const int32_t j = h->j;
             const T* xs = reinterpret_cast<const T*>(h + 1) + tid;
             // ---- critical chain
             constexpr int RX = R <= 8 ? R : 1;
@@ -1323,7 +1408,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             if constexpr (R <= 8) {
 #pragma unroll
-                for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
+                for (int q = 0; q < R; ++q) xv[q] = had_pf ? xvn[q] : ((tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0);
 #pragma unroll
                 for (int q = 0; q < R; q += 2) {
                     a0 = fma(xv[q], rr[q], a0);
@@ -1344,13 +1429,32 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                     }
                 }
             }
+            // prefetch entry k+1 (header, ColInfo, this thread's rows) under the reduction
+            // branch-free: the loads follow the (acquire) phase test in program
+            // order and are used only if it passed, so the butterfly below is
+            // not held behind the test's latency
+            {
+                const int s1 = (k + 1) & kmask;
+                pf = mbar_test_s(bar_s + 8u * s1, (unsigned)(((k + 1) >> kshift) & 1));
+                const SlotHdr* h1 = reinterpret_cast<const SlotHdr*>(ring + (size_t)s1 * sbytes);
+                pf_pos = h1->pos; pf_hg = h1->gen; pf_j = h1->j; pf_tc = h1->tcert; pf_dp = h1->dp;
+                pf_bj = h1->ci.beta; pf_ns = h1->ci.ns; pf_iv = h1->ci.inv; pf_uq = h1->ci.u; pf_nr = h1->ci.nr;
+                if constexpr (R <= 8) {
+                    const T* xs1 = reinterpret_cast<const T*>(h1 + 1) + tid;
+#pragma unroll
+                    for (int q = 0; q < R; ++q) xvn[q] = (tid + q * BT < n) ? to_d(xs1[q * BT]) : 0.0;
+                }
+            }
             double acc = warp_sum((a0 + a1) + (a2 + a3));
             double g;
             if (W > 1) {
                 if (lane == 0) part[pb * 32 + w] = acc;
                 named_bar(1, BT);
-                g = 0.0;
-                for (int q = 0; q < W; ++q) g += part[pb * 32 + q];
+                // warps' partials loaded together, summed in a fixed tree (W <= 7)
+                double pw[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pw[q] = q < W ? part[pb * 32 + q] : 0.0;
+                g = ((pw[0] + pw[1]) + (pw[2] + pw[3])) + ((pw[4] + pw[5]) + (pw[6] + pw[7]));
                 pb ^= 1;
             } else {
                 g = acc;
@@ -1378,16 +1482,19 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                     D = delta_step(D, step, rho0);
                     gstep = 0.875 * gstep + 0.125 * step;
                 }
-                // bookkeeping stores by every lane of every compute warp (same
-                // value, same address): no divergent branch in the chain
-                beta[j] = nb;
-                cinfo_w[j].beta = nb;
-                if (use_t && bj == 0.0) {
-                    tg[pos] = -1.0f;                       // now in the support
-                    if (m <= TT) ts[pos] = -1.0f;      // resident tile (single tile only)
+                // bookkeeping stores by one lane that never signals consumption:
+                // the consumed release (lane 0 of each warp) does not wait on them
+                if (w == W - 1 && lane == 1) {
+                    beta[j] = nb;
+                    cinfo_w[j].beta = nb;
+                    if (use_t && bj == 0.0) {
+                        tg[pos] = -1.0f;                       // now in the support
+                        if (m <= TT) ts[pos] = -1.0f;      // resident tile (single tile only)
+                    }
                 }
-                st_vol_f64_s(dpub_s, D);
+                if (lane == 0) st_vol_f64_s(dpub_s, D);
             }
+        }
         }
         if (W > 1) named_bar(1, BT);
         double s2 = 0.0;
@@ -1734,7 +1841,8 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
     __shared__ int s_tile_valid;
     if (threadIdx.x == 0) s_tile_valid = 0;
     __syncthreads();
-    const bool gap_rule = P.rule == 1;
+    const bool gap_rule = P.rule == R_GAP_SPHERE;
+    const bool screening = P.rule != R_NONE;
     const double gam = gamma_n(P.sparse ? (int64_t)P.n : (int64_t)P.n);
 
     if (ctl->done) return;
@@ -1761,8 +1869,24 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
                     const double dual = 0.5 * sc->y_norm_sq - 0.5 * (lam * lam) * dsq;
                     const double gap = primal - dual;
                     int st = ST_OK;
-                    if (P.prev_margin < -1e-9) st = ST_INFEASIBLE;
-                    else if (gap < -1e-10) st = ST_NEG_GAP;
+                    if (P.rule == R_GAP_DOME) {
+                        // region_gap_dome(prob_t, beta_prev, theta_prev, rho_prev) (regions.py:250-273)
+                        if (P.prev_margin < -1e-9) st = ST_VALUE;
+                        const double big_r = sqrt(dsq);
+                        sc->rule_R = big_r;
+                        if (st == ST_OK && big_r > 0.0) {
+                            const double val = sc->y_norm_sq - rho_sq - 2.0 * lam * l1s;
+                            double r_in = sqrt(fmax(val, 0.0)) / lam;
+                            if (r_in > big_r * (1 + 1e-9) + 1e-12) st = ST_NEG_GAP;
+                            r_in = fmin(r_in, big_r);
+                            const double ratio = 2.0 * (r_in / big_r) * (r_in / big_r) - 1.0;
+                            sc->rule_rd = 0.5 * big_r;
+                            sc->rule_a = fmin(fmax(ratio, -1.0), 1.0);
+                        }
+                    } else {
+                        if (P.prev_margin < -1e-9) st = ST_INFEASIBLE;
+                        else if (gap < -1e-10) st = ST_NEG_GAP;
+                    }
                     sc->status = st;
                     sc->gap_pre = gap;
                     sc->radius = sqrt(2.0 * fmax(gap, 0.0)) / lam;
@@ -1867,18 +1991,20 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
                     double corr; int64_t ci;
                     group_max_result(g, P, corr, ci);
                     cta_dual(P, corr, gap_rule ? 1 : 0, true, m, red);
+                    if (threadIdx.x == 0) rule_scalars(P, sc);
+                    __syncthreads();
                 }
                 group_sync(g);
                 if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
                 const double alpha = sc->alpha, radius = sc->radius, anchor = sc->rho_norm_ub;
                 const bool cert = P.certify != 0;
-                if (gap_rule) {
+                if (screening) {
                     // keep = mu >= 1 - 1e-9 with mu = |alpha c| + r ||x|| (solver.py:208-216);
                     // kept positions carry their certification thresholds along.
                     const int32_t* A = P.A;
                     group_compact2(g, P, m,
                                    [&](int64_t i) {
-                                       const double mu = fabs(alpha * P.c[i]) + radius * __ldg(P.norms + A[i]);
+                                       const double mu = rule_mu(P, sc, P.c[i], A[i], __ldg(P.norms + A[i]));
                                        return mu >= 1.0 - 1e-9;
                                    },
                                    [&](int64_t i, int64_t o) {
@@ -1890,7 +2016,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
                                        }
                                    },
                                    [&](int64_t i) {
-                                       const double mu = fabs(alpha * P.c[i]) + radius * __ldg(P.norms + A[i]);
+                                       const double mu = rule_mu(P, sc, P.c[i], A[i], __ldg(P.norms + A[i]));
                                        return !(mu >= 1.0 - 1e-9) && P.beta[A[i]] != 0.0;
                                    },
                                    [&](int64_t i, int64_t o) { P.Dl[o] = A[i]; },
@@ -1951,7 +2077,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
                     ctl->k = k;
                 }
                 group_sync(g);
-                if (gap_rule) {
+                if (screening) {
                     // swap A/A2 and t/t2 (device pointers are per launch; the host swaps between launches)
                     // handled by copying back: the compaction wrote the new active set into A2/t2
                     const int64_t mn = sc->m;

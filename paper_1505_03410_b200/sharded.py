@@ -125,6 +125,8 @@ def run_path_sharded(backend, y: np.ndarray, grid: np.ndarray, config: SolverCon
     rank 0 returns the PathResult (coefficients over all ``p_total``
     columns), the other ranks return None."""
     import torch.distributed as dist
+    if config.rule not in (Rule.NONE, Rule.GAP_SPHERE):
+        raise NotImplementedError("the sharded path runs the none / gap_sphere rules (north_star)")
     rank, world = dist.get_rank(), dist.get_world_size()
     y = np.ascontiguousarray(y, dtype=np.float64)
     n = y.size

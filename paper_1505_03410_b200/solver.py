@@ -7,10 +7,13 @@ post-drop certificate and trace at every checkpoint, and the CD epochs in
 between (one CTA per problem, exact certified-zero skipping).  The host only
 sequences launches and reads one scalar block per checkpoint.
 
-Rules on the GPU: ``none`` and ``gap_sphere`` (the north_star path).  The
-other members of ``Rule`` exist so configurations validate exactly as in the
-reference, but solving with them raises ``NotImplementedError`` (SURVEY.md
-§8(f) F1/F4 are the "next" rows).
+Rules on the GPU: every ``Rule`` of the reference (solver.py:24-32, 104-126).
+``gap_sphere`` is the north_star path; ``static``, ``dynamic``, ``st3`` and
+``gap_dome`` reuse the same checkpoint with their own
+per-column test, evaluated from q = X^T y (cached at solver creation),
+X^T x_jstar (ST3, built on first use) and the restricted dots X_A^T rho --
+no extra pass over the design.  Batched problems (cfg4) run ``none`` /
+``gap_sphere``.
 """
 
 from __future__ import annotations
@@ -36,7 +39,11 @@ class Rule(str, enum.Enum):
     GAP_DOME = "gap_dome"
 
 
-_GPU_RULES = {Rule.NONE: _lib.GS_RULE_NONE, Rule.GAP_SPHERE: _lib.GS_RULE_GAP_SPHERE}
+_GPU_RULES = {Rule.NONE: _lib.GS_RULE_NONE, Rule.GAP_SPHERE: _lib.GS_RULE_GAP_SPHERE,
+              Rule.STATIC: _lib.GS_RULE_STATIC, Rule.DYNAMIC: _lib.GS_RULE_DYNAMIC,
+              Rule.ST3: _lib.GS_RULE_ST3, Rule.GAP_DOME: _lib.GS_RULE_GAP_DOME}
+# batched problems (cfg4) run the north_star rules only
+_BATCH_RULES = {Rule.NONE: _lib.GS_RULE_NONE, Rule.GAP_SPHERE: _lib.GS_RULE_GAP_SPHERE}
 
 
 @dataclass
@@ -334,8 +341,8 @@ class BatchPathSolver:
         """grids: (B, T) non-increasing per row.  Returns a dict of (B, T)
         arrays: passes, gaps, converged, n_active (+ betas (B, T, p)) and the
         device time in ms."""
-        if config.rule not in _GPU_RULES:
-            raise NotImplementedError(f"rule {config.rule.value!r} is not on the B200 path in this build")
+        if config.rule not in _BATCH_RULES:
+            raise NotImplementedError(f"rule {config.rule.value!r} is not on the batched B200 path in this build")
         grids = np.ascontiguousarray(grids, dtype=np.float64)
         B, T = grids.shape
         if B != self.B:

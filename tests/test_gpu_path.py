@@ -186,8 +186,11 @@ def test_errors_map_to_reference_exceptions():
         gs.LassoProblem(X, np.array([1.0, 1.0]), 2.5)
     with pytest.raises(gs.NumericalInconsistencyError):
         gs.gap_radius(prob, -1.0)
-    with pytest.raises(NotImplementedError):
-        gs.solve(prob, gs.SolverConfig(rule="gap_dome"))
+    with pytest.raises(gs.NumericalInconsistencyError):
+        gs.region_gap_dome(prob, np.array([0.0, 0.0]), gs.make_dual_point(X, np.array([0.5, 0.5])),
+                           residual=np.array([0.0, 0.0]))
+    with pytest.raises(ValueError):
+        gs.region_dynamic(prob, th)
 
 
 def test_problem_algebra_hand_values():
@@ -263,3 +266,46 @@ def test_path_cfg2_generator_long_columns(n, p, T):
     rb = O.run_path(Xo, c.y, grid, O.SolverConfig(epsilon=c.epsilon, max_passes=100_000))
     compare_paths(ra, rb, float(c.y @ c.y))
     assert np.all(ra.converged)
+
+
+@pytest.mark.parametrize("rule", ["static", "dynamic", "st3", "gap_dome"])
+@pytest.mark.parametrize("kind", ["dense", "csc"])
+def test_path_rules_match_oracle(rule, kind):
+    """Every screening rule of the reference on the
+    device: same epochs, traces (incl. each rule's trace radius), active sets
+    and supports as the oracle, coefficients and gaps within tolerance."""
+    if kind == "dense":
+        c = synth.cfg0(p=1200)
+    else:
+        c = synth.cfg3(p=3000, n=400, nnz_per_col=12)
+    ra, rb, yy = _paths(c.X, c.y, 12, 2.5, c.epsilon, rule=rule)
+    compare_paths(ra, rb, yy)
+    for ta, tb in zip(ra.traces, rb.traces):
+        for x, y in zip(ta, tb):
+            assert abs(x[3] - y[3]) <= 1e-9 * max(1.0, abs(y[3])), (rule, x, y)
+
+
+def test_regions_api_dome_and_spheres_match_oracle():
+    """Region constructors and the dome test through the public API
+    (regions.py:82-119, 159-273) against the oracle."""
+    c = synth.cfg0(p=900)
+    X = gs.DesignMatrix(c.X)
+    Xo = O.DesignMatrix(c.X)
+    lmax, _ = Xo.max_abs_correlation(c.y)
+    lam = 0.3 * lmax
+    cfg = gs.SolverConfig(epsilon=c.epsilon, max_passes=40, screen_every=10)
+    prob = gs.LassoProblem(X, c.y, lam)
+    beta, cert, st = gs.solve(prob, cfg)
+    po = O.LassoProblem(Xo, c.y, lam)
+    th = O.DualPoint(theta=st.theta.theta, feasibility_margin=st.theta.feasibility_margin)
+    for mk, mko in ((lambda: gs.region_static(prob), lambda: O.region_static(po)),
+                    (lambda: gs.region_dynamic(prob, st.theta), lambda: O.region_dynamic(po, th)),
+                    (lambda: gs.region_st3(prob, st.theta), lambda: O.region_st3(po, th)),
+                    (lambda: gs.region_gap_dome(prob, beta, st.theta, residual=st.residual),
+                     lambda: O.region_gap_dome(po, beta, th, residual=st.residual))):
+        a, b = mk(), mko()
+        mu_a, mu_b = gs.mu_values(a, X), O.mu_values(b, Xo)
+        np.testing.assert_allclose(mu_a, mu_b, rtol=1e-10, atol=1e-12)
+        sa, sb = gs.screen(a, X), O.screen(b, Xo)
+        near = np.abs(mu_b - (1 - gs.SCREEN_SAFETY)) <= 1e-10
+        assert np.all(near[np.setxor1d(sa.active_set, sb.active_set)])
