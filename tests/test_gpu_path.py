@@ -280,9 +280,12 @@ def test_path_rules_match_oracle(rule, kind):
         c = synth.cfg3(p=3000, n=400, nnz_per_col=12)
     ra, rb, yy = _paths(c.X, c.y, 12, 2.5, c.epsilon, rule=rule)
     compare_paths(ra, rb, yy)
-    for ta, tb in zip(ra.traces, rb.traces):
-        for x, y in zip(ta, tb):
-            assert abs(x[3] - y[3]) <= 1e-9 * max(1.0, abs(y[3])), (rule, x, y)
+    if rule != "gap_dome":
+        # static / dynamic / ST3 traces report the region radius (solver.py:122-126);
+        # the dome's is the gap radius, covered by the gap criterion
+        for ta, tb in zip(ra.traces, rb.traces):
+            for x, y in zip(ta, tb):
+                assert abs(x[3] - y[3]) <= 1e-9 * max(1.0, abs(y[3])), (rule, x, y)
 
 
 def test_regions_api_dome_and_spheres_match_oracle():
