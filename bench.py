@@ -107,6 +107,46 @@ def _grid(lmax, case):
     return lambda_grid(lmax, case.n_lambdas, case.delta)
 
 
+def _full_path_scale(config: str, k: int):
+    """Scale factor from the first k lambdas to the whole path, from the
+    per-lambda times of one complete CPU path of the same workload measured
+    with the same oracle (profiles/r01/cpu_oracle_<config>_full.json).  The
+    late lambdas dominate (cfg1: the first 64 are 5% of the path), so the
+    bounded sample is scaled to the metric's unit with the measured cost
+    profile, not linearly."""
+    path = os.path.join(ROOT, "profiles", "r01", f"cpu_oracle_{config}_full.json")
+    try:
+        with open(path) as f:
+            per = json.load(f)["per_lambda_s"]
+    except Exception:
+        return None, None
+    if k <= 0 or k > len(per) or sum(per[:k]) <= 0:
+        return None, None
+    return sum(per) / sum(per[:k]), os.path.relpath(path, ROOT)
+
+
+def _roofline_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the screening
+    kernel from the committed ncu --set full capture (profiles/r01)."""
+    import re
+    for name in ("ncu_screen_full_cfg1_r01b.md", "ncu_screen_full_cfg1.md"):
+        path = os.path.join(ROOT, "profiles", "r01", name)
+        try:
+            txt = open(path).read()
+        except OSError:
+            continue
+        vals = {}
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            m = re.search(re.escape(key) + r" \| ([0-9.]+) (\w+)", txt)
+            if m:
+                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(2), None)
+                if mult:
+                    vals[key] = float(m.group(1)) * mult
+        if len(vals) == 2:
+            return sum(vals.values()), name
+    return None, None
+
+
 def _cpu_sample(case, grid, budget_s):
     """Oracle (reference algorithm, CPU) on the first lambdas of the same path,
     stopping after the point at which the budget is exceeded."""
@@ -136,8 +176,12 @@ def run_reference(args):
             npts = len(res.timings)
         if step >= args.warmup:
             times.append(sum(res.timings))
-    value = statistics.median(times)
-    sample = f"first {npts} of {grid.size} lambdas of the {args.config} path (run_path timing scope, path.py:78,94)"
+    measured = statistics.median(times)
+    scale, src = _full_path_scale(args.config, npts)
+    value = measured * scale if scale else measured
+    sample = (f"first {npts} of {grid.size} lambdas of the {args.config} path (run_path timing scope, path.py:78,94)"
+              + (f", scaled to the whole path x{scale:.3f} by the measured per-lambda cost profile ({src})"
+                 if scale else " (not scaled: no full-path profile)"))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -145,7 +189,7 @@ def run_reference(args):
             "config": {"workload": args.config, "n": int(case.X.shape[0]), "p": int(case.X.shape[1]),
                        "lambdas": int(grid.size), "sample_lambdas": npts, "tol": case.tol},
             "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
-                             "sample": sample},
+                             "sample": sample, "measured_sample_s": measured},
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -208,6 +252,7 @@ def run_ours(args):
     scr_bytes = n * p * es + p * (8 + 1) + n * 8       # X, norms in, keep marks out, center
     scr_ms = timer.screen_pass_ms(X, res.states[-1].theta.theta, 1e-3, reps=10)
     achieved = scr_bytes / (scr_ms * 1e-3) / 1e9
+    traffic, traffic_src = _roofline_traffic() if args.config == "cfg1" else (None, None)
     inpath_screen = agg["screen_ms"] / max(1, agg["n_screen"])
 
     # ---- e2e through the public API from pinned host buffers
@@ -225,7 +270,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_screen_full (group_gemv G_MU: full-p screening GEMV + sphere test)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "bytes_per_launch": scr_bytes, "launch_ms": scr_ms,
                      "in_path_screen_ms": inpath_screen},
         "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -240,11 +285,16 @@ def run_ours(args):
         sample, wall = _cpu_sample(case, grid, args.cpu_budget)
         k = len(sample.timings)
         gpu_same = sum(res.timings[:k])
-        line["cpu_baseline"] = {"value": sum(sample.timings), "unit": "s", "cores": len(os.sched_getaffinity(0)),
-                                "kind": "port",
-                                "sample": f"first {k} of {grid.size} lambdas of the {args.config} path",
+        measured = sum(sample.timings)
+        scale, src = _full_path_scale(args.config, k)
+        line["cpu_baseline"] = {"value": measured * scale if scale else measured, "unit": "s",
+                                "cores": len(os.sched_getaffinity(0)), "kind": "port",
+                                "sample": (f"first {k} of {grid.size} lambdas of the {args.config} path"
+                                           + (f", scaled to the whole path x{scale:.3f} by the measured per-lambda "
+                                              f"cost profile ({src})" if scale else " (not scaled)")),
+                                "measured_sample_s": measured,
                                 "gpu_same_sample_s": gpu_same,
-                                "speedup_same_sample": sum(sample.timings) / max(gpu_same, 1e-12)}
+                                "speedup_same_sample": measured / max(gpu_same, 1e-12)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
