@@ -312,3 +312,22 @@ def test_regions_api_dome_and_spheres_match_oracle():
         sa, sb = gs.screen(a, X), O.screen(b, Xo)
         near = np.abs(mu_b - (1 - gs.SCREEN_SAFETY)) <= 1e-10
         assert np.all(near[np.setxor1d(sa.active_set, sb.active_set)])
+
+
+def test_elastic_net_pure_l1_and_kkt():
+    """elastic_net.py: the pure-l1 reduction is the plain Lasso, and a converged
+    path point satisfies the KKT conditions to the gap tolerance; the implicit
+    tail (F2) is refused loudly."""
+    c = synth.cfg0(p=700)
+    X = gs.DesignMatrix(c.X)
+    lmax, _ = X.max_abs_correlation(c.y)
+    en = gs.ElasticNetProblem(X, c.y, 0.2 * lmax, 1.0)
+    prob = gs.to_lasso(en)
+    assert prob.lam == 0.2 * lmax and prob.X is X
+    beta, cert, st = gs.solve(prob, gs.SolverConfig(epsilon=1e-12 * float(c.y @ c.y), max_passes=100_000))
+    assert st.converged
+    assert gs.kkt_residual(en, beta) <= 1e-5 * prob.lam
+    ob = gs.objective(en, beta)
+    assert abs(ob - cert.primal) <= 1e-9 * abs(ob)
+    with pytest.raises(NotImplementedError):
+        gs.to_lasso(gs.ElasticNetProblem(X, c.y, 0.2 * lmax, 0.5))
