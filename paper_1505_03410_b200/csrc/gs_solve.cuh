@@ -2230,11 +2230,9 @@ struct BatchOut {
 };
 
 template <typename T, int R>
-__global__ void __launch_bounds__(256, 1) k_batch_path(SolveDev* probs, const BatchOut* outs) {
-    extern __shared__ __align__(16) unsigned char smem[];
+static __device__ void batch_problem(SolveDev* probs, const BatchOut* outs, const int b, unsigned char* smem) {
     __shared__ SolveDev sp;
     __shared__ int sh[32];
-    const int b = blockIdx.x;
     if (threadIdx.x == 0) sp = probs[b];
     __syncthreads();
     const BatchOut& o = outs[b];
@@ -2308,6 +2306,25 @@ __global__ void __launch_bounds__(256, 1) k_batch_path(SolveDev* probs, const Ba
             double* dst = o.betas + (int64_t)t * p;
             for (int64_t j = threadIdx.x; j < p; j += blockDim.x) dst[j] = sp.beta[j];
         }
+        __syncthreads();
+    }
+}
+
+// Persistent batched driver: min(B, #SM) CTAs claim problems from a global
+// counter, so long and short bootstrap paths pack dynamically instead of in
+// static waves of one problem per CTA.  Each problem's arithmetic does not
+// depend on which CTA runs it (results are bit-identical to any schedule).
+template <typename T, int R>
+__global__ void __launch_bounds__(256, 1) k_batch_path(SolveDev* probs, const BatchOut* outs, int B, int* next) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_b;
+    for (;;) {
+        if (threadIdx.x == 0) s_b = atomicAdd(next, 1);
+        __syncthreads();
+        const int b = s_b;
+        __syncthreads();
+        if (b >= B) break;
+        batch_problem<T, R>(probs, outs, b, smem);
         __syncthreads();
     }
 }

@@ -35,8 +35,18 @@ cudaError_t batch_R(cudaStream_t st, SolveDev* dprobs, const BatchOut* douts, in
     auto kern = k_batch_path<GS_T, R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)B, kThreads, smem, st>>>(dprobs, douts);
-    return cudaGetLastError();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int* next = nullptr;
+    e = cudaMallocAsync((void**)&next, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(next, 0, sizeof(int), st);
+    const int grid = B < sms ? B : sms;
+    kern<<<(unsigned)grid, kThreads, smem, st>>>(dprobs, douts, B, next);
+    e = cudaGetLastError();
+    cudaFreeAsync(next, st);
+    return e;
 }
 }  // namespace
 
