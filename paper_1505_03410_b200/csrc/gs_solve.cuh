@@ -1347,26 +1347,15 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 cd_consume_gram<T, R>(P, m, W, ring, sbytes, kmask, bar_s, kshift, cons_s, fin_s, reqg_s, reqp_s, dpub_s, cc,
                                       gw, ts, use_t, rho0, rr, D, gstep, n_unc, n_nz, n_req, n_cand, n_skip, tid);
         } else {
-        bool pf = false;                 // entry k was prefetched under entry k-1's reduction
-        int pf_pos = 0, pf_hg = 0, pf_j = 0;
-        double pf_tc = 0.0, pf_dp = 0.0, pf_bj = 0.0, pf_ns = 0.0, pf_iv = 0.0, pf_uq = 0.0, pf_nr = 0.0;
-        constexpr int RN = R <= 8 ? R : 1;
-        double xvn[RN];
-#pragma unroll
-        for (int q = 0; q < RN; ++q) xvn[q] = 0.0;
         for (int k = 0;; ++k) {
             const int s = k & kmask;
             // entries before k are fully read: consumed is signalled in batches (release store)
             if (k > 0 && (k & cmask) == 0) { __syncwarp(); if (lane == 0) st_rel_s(mycons_s, k); }
-            // one poll per entry (unless it was prefetched under the previous
-            // entry's reduction): header and bytes are published together
+            // one poll per entry: header and bytes are published together
             // through the slot mbarrier
             int pos, hg, j;
             double tc, dp, bj, ns, iv, uq, nr;
-            if (pf) {
-                pos = pf_pos; hg = pf_hg; j = pf_j; tc = pf_tc; dp = pf_dp;
-                bj = pf_bj; ns = pf_ns; iv = pf_iv; uq = pf_uq; nr = pf_nr;
-            } else {
+            {
                 const unsigned par = (unsigned)((k >> kshift) & 1);
                 if (!mbar_test_s(bar_s + 8u * s, par)) {
                     const unsigned long long t0 = gtimer();
@@ -1376,8 +1365,6 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 pos = h0->pos; hg = h0->gen; j = h0->j; tc = h0->tcert; dp = h0->dp;
                 bj = h0->ci.beta; ns = h0->ci.ns; iv = h0->ci.inv; uq = h0->ci.u; nr = h0->ci.nr;
             }
-            const bool had_pf = pf;
-            pf = false;
             const SlotHdr* h = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
             bool process = hg == gen && pos < m;
             if (hg == gen && use_t && D > dp) {
@@ -1408,7 +1395,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             if constexpr (R <= 8) {
 #pragma unroll
-                for (int q = 0; q < R; ++q) xv[q] = had_pf ? xvn[q] : ((tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0);
+                for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
 #pragma unroll
                 for (int q = 0; q < R; q += 2) {
                     a0 = fma(xv[q], rr[q], a0);
@@ -1427,22 +1414,6 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                         else if (u == 2) a2 = fma(x, r, a2);
                         else a3 = fma(x, r, a3);
                     }
-                }
-            }
-            // prefetch entry k+1 (header, ColInfo, this thread's rows) under the reduction
-            // branch-free: the loads follow the (acquire) phase test in program
-            // order and are used only if it passed, so the butterfly below is
-            // not held behind the test's latency
-            {
-                const int s1 = (k + 1) & kmask;
-                pf = mbar_test_s(bar_s + 8u * s1, (unsigned)(((k + 1) >> kshift) & 1));
-                const SlotHdr* h1 = reinterpret_cast<const SlotHdr*>(ring + (size_t)s1 * sbytes);
-                pf_pos = h1->pos; pf_hg = h1->gen; pf_j = h1->j; pf_tc = h1->tcert; pf_dp = h1->dp;
-                pf_bj = h1->ci.beta; pf_ns = h1->ci.ns; pf_iv = h1->ci.inv; pf_uq = h1->ci.u; pf_nr = h1->ci.nr;
-                if constexpr (R <= 8) {
-                    const T* xs1 = reinterpret_cast<const T*>(h1 + 1) + tid;
-#pragma unroll
-                    for (int q = 0; q < R; ++q) xvn[q] = (tid + q * BT < n) ? to_d(xs1[q * BT]) : 0.0;
                 }
             }
             double acc = warp_sum((a0 + a1) + (a2 + a3));
