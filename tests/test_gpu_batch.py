@@ -40,3 +40,23 @@ def test_batch_paths_match_oracle():
             assert np.array_equal(np.flatnonzero(res["betas"][b, t]), np.flatnonzero(st.beta)), (b, t)
             assert beta_close(res["betas"][b, t], st.beta), (b, t)
             assert gap_close(res["gaps"][b, t], st.cert.gap, yy), (b, t)
+
+
+def test_batch_more_problems_than_sms_schedule_independent():
+    """The persistent batch grid (min(B, #SM) CTAs claiming problems from a
+    counter) runs several problems per CTA when B > #SM; every problem's
+    epochs, gaps and active sets equal those of a batch holding it alone."""
+    X0, y0, _ = synth.cfg4_shared(p=1500)
+    B = 160
+    rows = np.stack([synth.cfg4_rows(b) for b in range(B)]).astype(np.int32)
+    D0 = gs.DesignMatrix(X0)
+    bs = gs.BatchPathSolver(D0, y0, rows)
+    grids = np.stack([gs.lambda_grid(bs.lambda_max[b], 6, 1.5) for b in range(B)])
+    cfg = gs.SolverConfig(epsilon=1e-8 * float(y0 @ y0) / 2, max_passes=100_000)
+    res = bs.run_paths(grids, cfg)
+    assert np.all(res["converged"])
+    for b in (0, 77, 148, 159):
+        one = gs.BatchPathSolver(D0, y0, rows[b:b + 1]).run_paths(grids[b:b + 1], cfg)
+        assert np.array_equal(one["passes"][0], res["passes"][b]), b
+        assert np.array_equal(one["gaps"][0], res["gaps"][b]), b
+        assert np.array_equal(one["n_active"][0], res["n_active"][b]), b
