@@ -85,6 +85,7 @@ static inline unsigned grid_for(int64_t n, int block, int64_t cap = 148 * 16) {
 struct gs_matrix {
     int sparse = 0, dtype = GS_DTYPE_F64;
     int64_t n = 0, p = 0, ld = 0, nnz = 0;
+    int64_t max_col_nnz = 0;                 // CSC: longest column
     void* X = nullptr;                       // dense
     double* data = nullptr;                  // CSC
     int32_t* indices = nullptr;
@@ -186,6 +187,7 @@ extern "C" int gs_matrix_csc(const double* data, const int32_t* indices, const i
     gs_matrix* M = new gs_matrix();
     M->sparse = 1; M->n = n; M->p = p;
     const int64_t nnz = indptr[p];
+    for (int64_t j = 0; j < p; ++j) M->max_col_nnz = std::max<int64_t>(M->max_col_nnz, indptr[j + 1] - indptr[j]);
     M->nnz = nnz;
     int rc;
     if ((rc = [&]() -> int {
@@ -568,6 +570,7 @@ struct gs_solver {
     int G = 1;
     double lmax = 0.0, y_norm_sq = 0.0;
     int64_t jstar = 0;
+    int* rowmark = nullptr;       // [n] row map of the parallel CSC waves
     double* q = nullptr;          // X^T y (static / dynamic / ST3 / dome centres)
     double* gstar = nullptr;      // X^T x_jstar (ST3), built on first use
     bool gstar_ready = false;
@@ -588,7 +591,7 @@ static void solver_release(gs_solver* S) {
     cudaFree(S->flags); cudaFree(S->mark); cudaFree(S->partial);
     cudaFree(S->sc); cudaFreeHost(S->hs); cudaFree(S->ctl); cudaFreeHost(S->hctl); cudaFree(S->bar);
     cudaFree(S->cta_val); cudaFree(S->cta_idx); cudaFree(S->cta_cnt); cudaFree(S->dprob); cudaFree(S->trace);
-    cudaFree(S->q); cudaFree(S->gstar);
+    cudaFree(S->q); cudaFree(S->gstar); cudaFree(S->rowmark);
     S->s.release();
     if (S->ev0) cudaEventDestroy(S->ev0);
     if (S->ev1) cudaEventDestroy(S->ev1);
@@ -659,6 +662,10 @@ extern "C" int gs_solver_create(const gs_matrix* M, const double* y, gs_solver**
         TRY(sc_upload(S));
         // lambda_max = |X^T y|_inf, j_star (problem.py:50), ||y||^2 (problem.py:54)
         TRY(dalloc(&S->q, p));
+        if (M->sparse) {
+            TRY(dalloc(&S->rowmark, n + 1));
+            CK(cudaMemsetAsync(S->rowmark, 0x7f, (n + 1) * sizeof(int), S->st));
+        }
         GemvArgs a{};
         a.v = S->y; a.m = p; a.mode = GEMV_MAX; a.blk_val = S->s.blk_val; a.blk_idx = S->s.blk_idx;
         a.out_c = S->q;                    // X^T y kept for the static/dynamic/ST3/dome centres
@@ -793,6 +800,12 @@ static void fill_dev(gs_solver* S, SolveDev& d) {
     const char* ep = getenv("GS_CD_PROF");
     d.cd_prof = ep ? atoi(ep) : 0;
     d.q = S->q; d.gstar = S->gstar; d.lmax_path = S->lmax; d.jstar = S->jstar;
+    d.rowmark = S->rowmark;
+    // CSC waves: fully parallel when rows are plentiful relative to column
+    // length (conflicts between a wave's members are rare); otherwise the
+    // conflict-free admission (profiles/r01/cd_modes.md)
+    const char* ec = getenv("GS_CSC_PAR");
+    d.csc_par = ec ? atoi(ec) : (M->sparse && M->n >= 256 * std::max<int64_t>(M->max_col_nnz, 1) ? 1 : 0);
 }
 
 // column j of the design as a dense f64 n-vector (regions.py:187: X.matvec(e_j))

@@ -118,6 +118,8 @@ struct SolveDev {
     double lmax_path;
     int64_t jstar;
     int cd_prof;         // print Gram-window phase cycles at the end of each solve (debug)
+    int csc_par;         // CSC CD: fully parallel waves (cd_epoch_csc_par)
+    int* rowmark;        // [n] row map of cd_epoch_csc_par (kRowFree between waves)
 };
 
 struct Group {
@@ -1347,15 +1349,28 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 cd_consume_gram<T, R>(P, m, W, ring, sbytes, kmask, bar_s, kshift, cons_s, fin_s, reqg_s, reqp_s, dpub_s, cc,
                                       gw, ts, use_t, rho0, rr, D, gstep, n_unc, n_nz, n_req, n_cand, n_skip, tid);
         } else {
+        bool pf = false;                 // entry k was prefetched under entry k-1's reduction
+        int pf_pos = 0, pf_hg = 0, pf_j = 0;
+        double pf_tc = 0.0, pf_dp = 0.0, pf_bj = 0.0, pf_ns = 0.0, pf_iv = 0.0, pf_uq = 0.0, pf_nr = 0.0;
+        constexpr int RN = R <= 8 ? R : 1;
+        double xvn[RN];
+#pragma unroll
+        for (int q = 0; q < RN; ++q) xvn[q] = 0.0;
         for (int k = 0;; ++k) {
             const int s = k & kmask;
             // entries before k are fully read: consumed is signalled in batches (release store)
             if (k > 0 && (k & cmask) == 0) { __syncwarp(); if (lane == 0) st_rel_s(mycons_s, k); }
-            // one poll per entry: header and bytes are published together
+            // one poll per entry (unless it was prefetched under the previous
+            // entry's reduction): header and bytes are published together
             // through the slot mbarrier
             int pos, hg, j;
             double tc, dp, bj, ns, iv, uq, nr;
-            {
+            const bool had_pf = pf;
+            pf = false;
+            if (had_pf) {
+                pos = pf_pos; hg = pf_hg; j = pf_j; tc = pf_tc; dp = pf_dp;
+                bj = pf_bj; ns = pf_ns; iv = pf_iv; uq = pf_uq; nr = pf_nr;
+            } else {
                 const unsigned par = (unsigned)((k >> kshift) & 1);
                 if (!mbar_test_s(bar_s + 8u * s, par)) {
                     const unsigned long long t0 = gtimer();
@@ -1395,7 +1410,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             if constexpr (R <= 8) {
 #pragma unroll
-                for (int q = 0; q < R; ++q) xv[q] = (tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0;
+                for (int q = 0; q < R; ++q) xv[q] = had_pf ? xvn[q] : ((tid + q * BT < n) ? to_d(xs[q * BT]) : 0.0);
 #pragma unroll
                 for (int q = 0; q < R; q += 2) {
                     a0 = fma(xv[q], rr[q], a0);
@@ -1414,6 +1429,24 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                         else if (u == 2) a2 = fma(x, r, a2);
                         else a3 = fma(x, r, a3);
                     }
+                }
+            }
+            // prefetch entry k+1 (header, ColInfo, this thread's rows) under the
+            // reduction.  The slot address is selected by the phase test's
+            // result: the loads are data-dependent on the (acquire) test, so
+            // they cannot observe the slot before its phase completed, and no
+            // branch holds the butterfly below behind the test's latency.
+            {
+                const int s1 = (k + 1) & kmask;
+                pf = mbar_test_s(bar_s + 8u * s1, (unsigned)(((k + 1) >> kshift) & 1));
+                const int sl = pf ? s1 : s;
+                const SlotHdr* h1 = reinterpret_cast<const SlotHdr*>(ring + (size_t)sl * sbytes);
+                pf_pos = h1->pos; pf_hg = h1->gen; pf_j = h1->j; pf_tc = h1->tcert; pf_dp = h1->dp;
+                pf_bj = h1->ci.beta; pf_ns = h1->ci.ns; pf_iv = h1->ci.inv; pf_uq = h1->ci.u; pf_nr = h1->ci.nr;
+                if constexpr (R <= 8) {
+                    const T* xs1 = reinterpret_cast<const T*>(h1 + 1) + tid;
+#pragma unroll
+                    for (int q = 0; q < R; ++q) xvn[q] = (tid + q * BT < n) ? to_d(xs1[q * BT]) : 0.0;
                 }
             }
             double acc = warp_sum((a0 + a1) + (a2 + a3));
@@ -1521,6 +1554,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
 // old rho values are restored) and the next wave starts at that position.
 constexpr int kSpTile = 4096;    // thresholds + positions staged per tile
 constexpr int kSpMW = 32;        // members per wave (one per lane of warp 0)
+constexpr int kRowFree = 0x7f7f7f7f;   // row map value between waves (cudaMemset 0x7f)
 
 struct SpMember {
     int32_t pos, j, nnz, pad;
@@ -1768,6 +1802,283 @@ static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m64,
                     const int r = M.idx[lane];
                     if (!keep && M.d != 0.0) srho[r] = oldv[it];
                     atomicAnd(&bm[r >> 5], ~(1u << (r & 31)));
+                }
+                if (keep && M.d != 0.0 && lane == 0) {
+                    P.beta[M.j] = M.nb;
+                    if (use_t && M.bj == 0.0) { P.t[M.pos] = -1.0f; ts[M.pos - tb] = -1.0f; }
+                }
+            }
+            if (tid == 0) s_a = b;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ctl->cd_delta = s_D;
+        ctl->cd_gstep = gstep;
+        ctl->epoch_unc = n_unc;
+        ctl->epoch_nz = n_nz;
+        ctl->n_requeue += n_roll;
+        ctl->n_cand += n_mem;
+        P.sc->visits += (unsigned long long)m;
+        P.sc->uncertified += (unsigned long long)n_unc;
+        P.sc->nonzero += (unsigned long long)n_nz;
+    }
+    __syncthreads();
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int r = tid; r < n; r += blockDim.x) { const double q = srho[r]; P.rho[r] = q; s = __dadd_ru(s, __dmul_ru(q, q)); }
+    s = block_sum_ru(s, red);
+    if (tid == 0) P.sc->rho_norm_ub = __dsqrt_ru(s);
+    __syncthreads();
+}
+
+
+// CSC CD epoch, fully parallel waves (GS_CSC_PAR=1; experimental).
+//
+// Warp 0 admits the next (up to 32) candidates uncertified under dp with one
+// ballot per 32 positions (a column with more than 32 nonzeros ends the wave
+// before it, or runs alone).  All warps compute every member's g from the
+// wave-start rho and its update d without writing rho.  Nonzero members mark
+// their rows in a global row map (atomicMin of the member index); every member
+// then checks its rows in parallel: a member that touches a row marked by an
+// earlier nonzero member read a stale rho value, and the wave ends there.
+// Accepted nonzero members have pairwise disjoint rows, so their axpys are
+// applied in parallel -- the arithmetic is the sequential CD's, bit for bit.
+// The certification cut-off and the statistics are those of cd_epoch_csc.
+static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t m64, unsigned char* smem) {
+    SolveCtl* ctl = P.ctl;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
+    const int n = P.n, m = (int)m64;
+    const unsigned FULL = 0xffffffffu;
+    float* ts = reinterpret_cast<float*>(smem);
+    int32_t* As = reinterpret_cast<int32_t*>(smem + kSpTile * 4);
+    double* srho = reinterpret_cast<double*>(smem + kSpTile * 8);
+    const int nbw = (n + 31) / 32;
+    SpMember* mem = reinterpret_cast<SpMember*>(smem + ((size_t)kSpTile * 8 + (size_t)n * 8 + (size_t)nbw * 4 + 15) / 16 * 16);
+    int* first = P.rowmark;                      // n ints, kRowFree between waves
+    __shared__ double s_D;
+    __shared__ int s_a, s_b, s_nmem, s_solo, s_tb, s_tend;
+    __shared__ int s_flag[kSpMW];
+    __shared__ int64_t s_lo[kSpMW];
+    const bool use_t = P.certify != 0;
+    const double lam = P.lam;
+    const double rho0 = ctl->anchor_norm;
+    for (int r = tid; r < n; r += blockDim.x) srho[r] = P.rho[r];
+    if (tid == 0) { s_D = use_t ? ctl->cd_delta : 0.0; s_a = 0; s_tb = 0; s_tend = 0; }
+    double gstep = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * lam;
+    long long n_unc = 0, n_nz = 0, n_roll = 0, n_mem = 0;
+    __syncthreads();
+    while (s_a < m) {
+        const int a = s_a;
+        if (a >= s_tend) {
+            const int tb = a, tend = min(m, a + kSpTile);
+            for (int q = tb + tid; q < tend; q += blockDim.x) {
+                As[q - tb] = P.A[q];
+                ts[q - tb] = use_t ? P.t[q] : -1.0f;
+            }
+            __syncthreads();
+            if (tid == 0) { s_tb = tb; s_tend = tend; }
+            __syncthreads();
+        }
+        const int tb = s_tb, tend = s_tend;
+        // ---------------- admission (warp 0, one ballot per 32 positions) ----------------
+        if (w == 0) {
+            const double D = s_D;
+            const double dp = use_t ? __dadd_ru(D, __dmul_ru(2.0 * kSpMW, gstep)) : 0.0;
+            int nmem = 0, b = -1, solo = 0;
+            for (int base = a; b < 0; base += 32) {
+                if (base >= tend) { b = tend; break; }
+                const int q = base + lane;
+                const bool unc = q < tend && (!use_t || !(dp < (double)ts[q - tb]));
+                const unsigned mask = __ballot_sync(FULL, unc);
+                if (!mask) continue;
+                int cj = 0, cnz = 0;
+                int64_t clo = 0;
+                if (unc) {
+                    cj = As[q - tb];
+                    clo = __ldg(P.indptr + cj);
+                    cnz = (int)(__ldg(P.indptr + cj + 1) - clo);
+                }
+                unsigned take = mask;
+                const unsigned longm = __ballot_sync(FULL, unc && cnz > 32);
+                if (longm) {
+                    const int fl = __ffs(longm) - 1;
+                    const unsigned before = mask & ((1u << fl) - 1u);
+                    if (nmem == 0 && before == 0u) { take = 1u << fl; solo = 1; b = base + fl + 1; }
+                    else { take = before; b = base + fl; }
+                }
+                const int room = kSpMW - nmem;
+                if (__popc(take) >= room) {
+                    const int lb = (int)__fns(take, 0, room);
+                    take &= (lb == 31) ? FULL : ((2u << lb) - 1u);
+                    b = base + lb + 1;
+                }
+                if ((take >> lane) & 1u) {
+                    const int k = nmem + __popc(take & ((1u << lane) - 1u));
+                    SpMember& M = mem[k];
+                    M.pos = q; M.j = cj; M.nnz = cnz;
+                    M.ns = __ldg(P.nsq + cj); M.nr = __ldg(P.norms + cj); M.bj = P.beta[cj];
+                    s_lo[k] = clo;
+                }
+                nmem += __popc(take);
+            }
+            if (lane == 0) { s_b = b; s_nmem = nmem; s_solo = solo; }
+        }
+        __syncthreads();
+        const int nmem = s_nmem;
+        // ---------------- g and d of every member from the wave-start rho ----------------
+        double oldv[(kSpMW + 7) / 8];
+#pragma unroll
+        for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
+            oldv[it] = 0.0;
+            const int k = w + it * NW;
+            if (k >= nmem) continue;
+            SpMember& M = mem[k];
+            double g, x = 0.0, o = 0.0;
+            const int64_t lo = s_lo[k];
+            if (!s_solo) {
+                int r = -1;
+                if (lane < M.nnz) { r = __ldg(P.indices + lo + lane); x = __ldg(P.data + lo + lane); o = srho[r]; }
+                if (lane < 32) { M.idx[lane] = r; M.val[lane] = x; }
+                g = warp_sum(fma(x, o, 0.0));
+            } else {
+                const int64_t hi = lo + M.nnz;
+                double acc = 0.0;
+                for (int64_t q = lo + lane; q < hi; q += 32) acc = fma(__ldg(P.data + q), srho[__ldg(P.indices + q)], acc);
+                g = warp_sum(acc);
+            }
+            const double z = M.bj + g / M.ns;
+            const double u = lam / M.ns;
+            const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+            const double d = nb - M.bj;
+            oldv[it] = o;
+            __syncwarp();
+            if (lane == 0) { M.d = d; M.nb = nb; M.step = d != 0.0 ? __dmul_ru(fabs(d), M.nr) : 0.0; }
+        }
+        __syncthreads();
+        // ---------------- conflicts with earlier nonzero members (row map) ----------------
+        if (!s_solo && nmem > 1) {
+#pragma unroll
+            for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
+                const int k = w + it * NW;
+                if (k < nmem && mem[k].d != 0.0 && lane < mem[k].nnz) atomicMin(first + mem[k].idx[lane], k);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
+                const int k = w + it * NW;
+                if (k >= nmem) continue;
+                const bool hit = lane < mem[k].nnz && __ldcg(first + mem[k].idx[lane]) < k;
+                const unsigned hb = __ballot_sync(FULL, hit);
+                if (lane == 0) s_flag[k] = hb != 0u;
+            }
+            __syncthreads();
+            if (w == 0) {
+                const bool f = lane < nmem && s_flag[lane];
+                const unsigned fb = __ballot_sync(FULL, f);
+                if (fb) {
+                    const int cut = __ffs(fb) - 1;
+                    if (lane >= cut && lane < nmem) mem[lane].step = 0.0;
+                    __syncwarp();
+                    if (lane == 0) s_b = mem[cut].pos;
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+        }
+        // ---------------- drift bound, certification check, cut-off (warp 0) ----------------
+        if (w == 0) {
+            int b = s_b;
+            double Dn = 0.0;
+            if (use_t) {
+                const double D = s_D;
+                const double st = lane < nmem ? mem[lane].step : 0.0;
+                double incl = st;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double t = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl = __dadd_ru(incl, t);
+                }
+                const double S = __shfl_sync(FULL, incl, 31);
+                double excl = __shfl_up_sync(FULL, incl, 1);
+                if (lane == 0) excl = 0.0;
+                // per update: |d| ||x|| (1+1e-12) plus a rounding term u ||rho_new||,
+                // ||rho_new|| <= rho0 + Delta + 2 S (see delta_step)
+                const double err = __dmul_ru(2.3e-16, __dadd_ru(__dadd_ru(rho0, D), __dmul_ru(2.0, S)));
+                auto Dk = [&](int k, double ex) {     // bound before member k (ex = steps of members < k)
+                    return __dadd_ru(__dadd_ru(D, __dmul_ru(ex, 1.0 + 1e-12)), __dmul_ru((double)k, err));
+                };
+                Dn = Dk(nmem, S);
+                const double dp = __dadd_ru(D, __dmul_ru(2.0 * kSpMW, gstep));
+                if (Dn > dp) {
+                    // find the first skipped position whose certificate fails under its real drift
+                    int cut = -1;
+                    for (int base = a; base < b && cut < 0; base += 32) {
+                        const int s = base + lane;
+                        bool bad = false;
+                        if (s < b) {
+                            int k = 0;                         // members before s
+                            bool is_mem = false;
+                            for (int q = 0; q < nmem; ++q) {
+                                const int pq = mem[q].pos;
+                                k += pq < s ? 1 : 0;
+                                is_mem |= pq == s;
+                            }
+                            if (!is_mem) {
+                                double ex = 0.0;               // steps of the members before s
+                                for (int q = 0; q < k; ++q) ex = __dadd_ru(ex, mem[q].step);
+                                bad = !(Dk(k, ex) < (double)ts[s - tb]);
+                            }
+                        }
+                        const unsigned bb = __ballot_sync(FULL, bad);
+                        if (bb) cut = base + __ffs(bb) - 1;
+                    }
+                    if (cut >= 0) {
+                        b = cut;
+                        int k = 0;
+                        double ex = 0.0;
+                        for (int q = 0; q < nmem; ++q)
+                            if (mem[q].pos < cut) { ++k; ex = __dadd_ru(ex, mem[q].step); }
+                        Dn = Dk(k, ex);
+                        if (lane == 0) ++n_roll;
+                    }
+                }
+            }
+            // kept members: statistics and the step estimate
+            if (lane == 0) {
+                for (int q = 0; q < nmem; ++q) {
+                    if (mem[q].pos >= b) break;
+                    ++n_unc;
+                    if (mem[q].d != 0.0) { ++n_nz; gstep = 0.875 * gstep + 0.125 * mem[q].step; }
+                }
+                n_mem += nmem;
+                s_b = b;
+                if (use_t) s_D = Dn;
+            }
+            gstep = __shfl_sync(FULL, gstep, 0);
+        }
+        __syncthreads();
+        // ---------------- commit: accepted nonzero members (disjoint rows), release the row map ----------------
+        {
+            const int b = s_b;
+#pragma unroll
+            for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
+                const int k = w + it * NW;
+                if (k >= nmem) continue;
+                const SpMember& M = mem[k];
+                const bool keep = M.pos < b;
+                if (!s_solo) {
+                    if (lane < M.nnz && M.d != 0.0) {
+                        const int r = M.idx[lane];
+                        if (keep) srho[r] = __dsub_rn(oldv[it], __dmul_rn(M.d, M.val[lane]));
+                        if (nmem > 1) first[r] = kRowFree;
+                    }
+                } else if (keep && M.d != 0.0) {
+                    const int64_t lo = s_lo[k], hi = lo + M.nnz;
+                    for (int64_t q = lo + lane; q < hi; q += 32) {
+                        const int32_t rr = __ldg(P.indices + q);
+                        srho[rr] = __dsub_rn(srho[rr], __dmul_rn(M.d, __ldg(P.data + q)));
+                    }
                 }
                 if (keep && M.d != 0.0 && lane == 0) {
                     P.beta[M.j] = M.nb;
@@ -2090,7 +2401,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
         }
         if (g.c == 0) {
             const unsigned long long td0 = gtimer();
-            if (P.sparse) cd_epoch_csc(P, m, smem);
+            if (P.sparse) { if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, m, smem); else cd_epoch_csc(P, m, smem); }
             else cd_epoch_dense<T, R>(P, m, P.cd_warps, smem, &s_tile_valid);
             if (threadIdx.x == 0) {
                 ctl->t_cd += gtimer() - td0;

@@ -331,3 +331,14 @@ def test_elastic_net_pure_l1_and_kkt():
     assert abs(ob - cert.primal) <= 1e-9 * abs(ob)
     with pytest.raises(NotImplementedError):
         gs.to_lasso(gs.ElasticNetProblem(X, c.y, 0.2 * lmax, 0.5))
+
+
+@pytest.mark.parametrize("rule", ["gap_sphere", "gap_dome"])
+def test_path_sparse_parallel_waves(rule):
+    """CSC with rows plentiful relative to column length (n >= 256 x max column
+    nnz, the cfg3 regime): the fully parallel waves (row map conflicts, parallel
+    commit) against the oracle."""
+    c = synth.cfg3(p=4000, n=4000, nnz_per_col=8)
+    ra, rb, yy = _paths(c.X, c.y, 14, 2.0, c.epsilon, rule=rule)
+    compare_paths(ra, rb, yy)
+    assert np.all(ra.converged)
