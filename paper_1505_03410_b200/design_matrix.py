@@ -8,8 +8,16 @@ row-parallel residual resync.  Column norms are computed on the device.  Every
 method runs a CUDA kernel through the C ABI; host arrays are only the
 caller's inputs and outputs.
 
-Not in this build: the Elastic-Net implicit tail
-(``tail_weight > 0``) raises ``NotImplementedError``.
+Elastic-Net tail (design_matrix.py:54-65,100-158): with
+``tail_weight > 0`` the reference keeps the rows ``sqrt(tail_weight) I_p``
+implicit.  Here they are stored: the device copy is the CSC of
+``[X; sqrt(w) I_p]`` (one extra entry per column, row ``n_base + j``, last in
+its column since indices are sorted), so every device kernel -- the products,
+the persistent solve, the sparse CD waves -- runs unchanged on the augmented
+problem.  The tail entry is the last term of each column's sequential sum,
+which is the reference's order (``s += tail_scale * v[n_base + j]`` after the
+base dot, _kernels.py tdot_*/cd_pass_*).  Column norms are the reference's
+``base_sq + tail_weight`` (:56), passed to the device, not recomputed.
 """
 
 from __future__ import annotations
@@ -28,10 +36,6 @@ class DesignMatrix:
     def __init__(self, storage, tail_weight: float = 0.0):
         if tail_weight < 0:
             raise ValueError("tail_weight must be non-negative")
-        if tail_weight > 0:
-            raise NotImplementedError(
-                "Elastic-Net implicit tail (tail_weight > 0) is a 'next' row (SURVEY.md §8(f) F2) "
-                "and not part of this build")
         lib = _lib.load()
         handle = ctypes.c_void_p()
         if sp.issparse(storage):
@@ -67,12 +71,32 @@ class DesignMatrix:
                                            self.n_cols, self.n_base, None, ctypes.byref(handle)))
         self._h = handle
         self._lib = lib
-        self.tail_weight = 0.0
-        self.tail_scale = 0.0
+        self.tail_weight = float(tail_weight)
+        self.tail_scale = float(np.sqrt(tail_weight))
         nsq = np.empty(self.n_cols, dtype=np.float64)
         _lib.check(lib.gs_matrix_norms_sq(self._h, _lib.f64p(nsq)))
+        if self.tail_weight > 0.0:
+            nsq = nsq + self.tail_weight                          # design_matrix.py:56
+            self._h = self._upload_augmented(nsq)
+            lib.gs_matrix_free(handle)
+            self.dtype = np.float64
         self._col_norms_sq = nsq
         self._col_norms = np.sqrt(nsq)
+
+    def _upload_augmented(self, nsq: np.ndarray) -> ctypes.c_void_p:
+        """Device CSC of [X; tail_scale I_p] with the reference's norms."""
+        base = self._mat if self.is_sparse else sp.csc_matrix(np.asarray(self._mat, dtype=np.float64))
+        tail = sp.identity(self.n_cols, dtype=np.float64, format="csc") * self.tail_scale
+        aug = sp.vstack([base, tail], format="csc")
+        aug.sort_indices()
+        self._aug_indptr64 = np.ascontiguousarray(aug.indptr, dtype=np.int64)
+        data = np.ascontiguousarray(aug.data, dtype=np.float64)
+        indices = np.ascontiguousarray(aug.indices, dtype=np.int32)
+        handle = ctypes.c_void_p()
+        _lib.check(self._lib.gs_matrix_csc(_lib.f64p(data), _lib.i32p(indices), _lib.i64p(self._aug_indptr64),
+                                           self.n_base + self.n_cols, self.n_cols, _lib.f64p(nsq),
+                                           ctypes.byref(handle)))
+        return handle
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -91,6 +115,9 @@ class DesignMatrix:
     # ------------------------------------------------------------------
     @property
     def n_rows(self) -> int:
+        """Logical rows, the tail included (design_matrix.py:60-65)."""
+        if self.tail_weight > 0:
+            return self.n_base + self.n_cols
         return self.n_base
 
     @property
@@ -110,6 +137,8 @@ class DesignMatrix:
 
     def normalized(self) -> "DesignMatrix":
         """Copy with unit-norm columns (zero columns left untouched)."""
+        if self.tail_weight > 0:
+            raise ValueError("cannot normalize an augmented matrix")
         norms = self._col_norms.copy()
         norms[norms == 0.0] = 1.0
         if self.is_sparse:
@@ -193,6 +222,8 @@ class DesignMatrix:
     # ------------------------------------------------------------------
     def toarray(self) -> np.ndarray:
         base = self._mat.toarray() if self.is_sparse else np.array(self._mat, dtype=np.float64)
+        if self.tail_scale > 0.0:                               # design_matrix.py:177-183
+            return np.asfortranarray(np.vstack([base, self.tail_scale * np.eye(self.n_cols)]))
         return np.asfortranarray(base)
 
     def raw(self):

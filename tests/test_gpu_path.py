@@ -2,6 +2,8 @@
 (a bit-identical restatement of the reference, tests/test_oracle_golden.py),
 on the same seeded inputs.  See tests/parity.py for the criteria."""
 
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse as sp
@@ -316,8 +318,7 @@ def test_regions_api_dome_and_spheres_match_oracle():
 
 def test_elastic_net_pure_l1_and_kkt():
     """elastic_net.py: the pure-l1 reduction is the plain Lasso, and a converged
-    path point satisfies the KKT conditions to the gap tolerance; the implicit
-    tail (F2) is refused loudly."""
+    path point satisfies the KKT conditions to the gap tolerance."""
     c = synth.cfg0(p=700)
     X = gs.DesignMatrix(c.X)
     lmax, _ = X.max_abs_correlation(c.y)
@@ -329,8 +330,92 @@ def test_elastic_net_pure_l1_and_kkt():
     assert gs.kkt_residual(en, beta) <= 1e-5 * prob.lam
     ob = gs.objective(en, beta)
     assert abs(ob - cert.primal) <= 1e-9 * abs(ob)
-    with pytest.raises(NotImplementedError):
-        gs.to_lasso(gs.ElasticNetProblem(X, c.y, 0.2 * lmax, 0.5))
+
+
+def test_tail_behaves_like_stacked_identity():
+    """design_matrix.py:54-65,100-183 with tail_weight > 0 (test_design_matrix.py:135-150)."""
+    rng = np.random.default_rng(4)
+    base = rng.standard_normal((6, 4))
+    w = 0.7
+    for storage in (base, sp.csc_matrix(base)):
+        X = gs.DesignMatrix(storage, tail_weight=w)
+        explicit = np.vstack([base, np.sqrt(w) * np.eye(4)])
+        assert X.n_rows == 10 and X.tail_scale == float(np.sqrt(w))
+        np.testing.assert_allclose(X.toarray(), explicit, rtol=1e-15)
+        v = rng.standard_normal(10)
+        for j in range(4):
+            assert X.col_dot(j, v) == pytest.approx(explicit[:, j] @ v, rel=1e-12)
+        np.testing.assert_array_equal(X.col_norms_sq, np.einsum("ij,ij->j", base, base) + w)
+        b = rng.standard_normal(4)
+        np.testing.assert_allclose(X.matvec(b), explicit @ b, rtol=1e-13)
+        a = v.copy()
+        X.axpy_col(2, 0.5, a)
+        np.testing.assert_allclose(a, v + 0.5 * explicit[:, 2], rtol=1e-15)
+        with pytest.raises(ValueError):
+            X.normalized()
+
+
+def _stacked_oracle(Xh, y, tail):
+    """The reference's implicit-tail problem restated on the explicitly stacked
+    design: tail rows after the base rows (so every sequential sum adds the tail
+    term last, as _kernels.py does) and the reference norms base_sq + w (:56)."""
+    Xh = Xh.toarray() if sp.issparse(Xh) else np.asarray(Xh, dtype=np.float64)
+    p = Xh.shape[1]
+    Xo = O.DesignMatrix(np.vstack([Xh, np.sqrt(tail) * np.eye(p)]))
+    Xo.col_norms_sq = np.einsum("ij,ij->j", Xh, Xh) + tail
+    Xo.col_norms = np.sqrt(Xo.col_norms_sq)
+    return Xo, np.concatenate([y, np.zeros(p)])
+
+
+@pytest.mark.parametrize("alpha,sparse", [(0.5, False), (0.3, True), (0.7, False)])
+def test_elastic_net_tail_matches_oracle(alpha, sparse):
+    """F2: to_lasso with a tail (elastic_net.py:34-46) solved on the device
+    against the oracle on the stacked design, and the Elastic-Net KKT
+    conditions (test_acceptance.py:331-348: kkt <= 1e-8 at epsilon 1e-10)."""
+    c = synth.cfg0(p=400)
+    Xh = sp.csc_matrix(np.where(np.abs(c.X) > 0.05, c.X, 0.0)) if sparse else c.X
+    X = gs.DesignMatrix(Xh)
+    lmax, _ = X.max_abs_correlation(c.y)
+    en = gs.ElasticNetProblem(X, c.y, 0.15 * lmax / alpha, alpha)
+    prob = gs.to_lasso(en)
+    tail = (1.0 - alpha) * en.lam
+    assert prob.X.tail_weight == tail and prob.y.size == X.n_base + X.n_cols
+    cfg = gs.SolverConfig(epsilon=1e-10, max_passes=100_000)
+    beta, cert, st = gs.solve(prob, cfg)
+    assert st.converged and cert.gap <= 1e-10
+    assert gs.kkt_residual(en, beta) <= 1e-8
+    Xo, yo = _stacked_oracle(Xh, c.y, tail)
+    b2, c2, st2 = O.solve(O.LassoProblem(Xo, yo, prob.lam), O.SolverConfig(epsilon=1e-10, max_passes=100_000))
+    assert st.passes_done == st2.passes_done
+    np.testing.assert_array_equal(beta != 0, b2 != 0)
+    np.testing.assert_allclose(beta, b2, rtol=0, atol=1e-8 * max(1.0, float(np.max(np.abs(b2)))))
+    assert abs(cert.gap - c2.gap) <= 1e-8 * max(abs(c2.primal), 1.0)
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "enet_cfg0_p400.npz"))
+    k = [(0.5, False), (0.3, True), (0.7, False)].index((alpha, sparse))
+    assert st.passes_done == int(g[f"c{k}_passes"])
+    np.testing.assert_allclose(beta, g[f"c{k}_beta"], rtol=0, atol=1e-8 * max(1.0, float(np.max(np.abs(b2)))))
+
+
+def test_elastic_net_path_and_report(tmp_path):
+    """bench.py:153-182 per-lambda reduction, warm-started, on the device; and
+    run_benchmark with l1_ratio < 1 (test_bench_cli.py:87-92)."""
+    c = synth.cfg0(p=300)
+    X = gs.DesignMatrix(c.X)
+    lmax, _ = X.max_abs_correlation(c.y)
+    grid = gs.lambda_grid(lmax, 6, 2.0)
+    cfg = gs.SolverConfig(epsilon=1e-10, max_passes=100_000)
+    res = gs.run_enet_path(X, c.y, grid, cfg, 0.5)
+    assert res.converged.all()
+    for t, lam in enumerate(grid):
+        en = gs.ElasticNetProblem(X, c.y, float(lam) / 0.5, 0.5)
+        assert gs.kkt_residual(en, res.betas[t]) <= 1e-8
+    plain = gs.run_path(X, c.y, grid, cfg)
+    same = gs.run_enet_path(X, c.y, grid, cfg, 1.0)
+    assert np.array_equal(plain.betas, same.betas)
+    from paper_1505_03410_b200.report import RunConfig, run_benchmark
+    rep = run_benchmark(RunConfig(out_dir=str(tmp_path / "out"), rules=["gap_sphere"], epsilons=[1e-8],
+                                  grid_T=5, grid_delta=2.0, l1_ratio=0.5), X, c.y)
+    assert rep["summary"]["runs"][0]["n_converged"] == 5
 
 
 @pytest.mark.parametrize("rule", ["gap_sphere", "gap_dome"])

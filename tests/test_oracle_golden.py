@@ -145,3 +145,29 @@ def test_oracle_equals_reference_directly(seed, sparse):
         assert np.array_equal(a.betas, b.betas)
         assert [c.gap for c in a.certs] == [c.gap for c in b.certs]
         assert a.traces == b.traces
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_stacked_oracle_matches_reference_enet_golden(k):
+    """F2: the oracle on the explicitly stacked design [X; sqrt(w) I] with the
+    reference norms base_sq + w reproduces the reference's implicit-tail
+    Elastic-Net solve (tests/golden/make_golden_enet.py): same passes, gap and
+    beta (bit for bit dense; sparse within 1e-14, dense-vs-CSC base sums)."""
+    from make_golden_enet import CASES, inputs
+    g = np.load(os.path.join(GOLD, "enet_cfg0_p400.npz"))
+    alpha, sparse = CASES[k]
+    c, Xh = inputs(alpha, sparse)
+    Xd = Xh.toarray() if sparse else Xh
+    p = Xd.shape[1]
+    lam = float(g[f"c{k}_lam"])
+    tail = (1.0 - alpha) * lam
+    Xo = O.DesignMatrix(np.vstack([Xd, np.sqrt(tail) * np.eye(p)]))
+    Xo.col_norms_sq = np.einsum("ij,ij->j", Xd, Xd) + tail
+    Xo.col_norms = np.sqrt(Xo.col_norms_sq)
+    b, cert, st = O.solve(O.LassoProblem(Xo, np.concatenate([c.y, np.zeros(p)]), lam * alpha),
+                          O.SolverConfig(epsilon=1e-10, max_passes=100_000))
+    assert st.passes_done == int(g[f"c{k}_passes"])
+    if sparse:
+        np.testing.assert_allclose(b, g[f"c{k}_beta"], rtol=0, atol=1e-14)
+    else:
+        assert np.array_equal(b, g[f"c{k}_beta"]) and cert.gap == float(g[f"c{k}_gap"])
