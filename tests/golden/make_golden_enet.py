@@ -13,12 +13,7 @@ import numpy as np
 import scipy.sparse as sp
 
 ROOT = Path(__file__).resolve().parents[2]
-sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, str(ROOT))
-
-import gapsafe as R  # noqa: E402
-from gapsafe.elastic_net import ElasticNetProblem, to_lasso  # noqa: E402
-from gapsafe.solver import SolverConfig, solve  # noqa: E402
 
 from paper_1505_03410_b200 import synth  # noqa: E402
 
@@ -32,6 +27,12 @@ def inputs(alpha, sparse):
 
 
 def main():
+    # the reference is imported only here (generation time, build container)
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import gapsafe as R
+    from gapsafe.elastic_net import ElasticNetProblem, to_lasso
+    from gapsafe.solver import SolverConfig, solve
+
     out = {}
     for k, (alpha, sparse) in enumerate(CASES):
         c, Xh = inputs(alpha, sparse)

@@ -1,6 +1,7 @@
 """Diagnose the sparse-base Elastic-Net tail case on the B200 (F2)."""
 import sys
 sys.path.insert(0, "tests/golden")
+sys.path.insert(0, ".")
 import numpy as np
 import paper_1505_03410_b200 as gs
 from make_golden_enet import CASES, inputs
