@@ -368,6 +368,7 @@ static int matvec_dev(const gs_matrix* M, cudaStream_t st, TmpBuf& tb, const dou
     if (M->sparse) {
         k_resync_csr<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(M->csr_data, M->csr_cols, M->csr_rowptr, (int)n, dbeta, dy, dout);
         CKL();
+        CK(cudaStreamSynchronize(st));   // callers copy dout on another stream
         return GS_OK;
     }
     uint8_t* flags; int32_t* S; int64_t* cnt; double* partial;
