@@ -13,8 +13,12 @@ max over ranks.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 oracle port of /root/reference/pkg/src/gapsafe, bit-identical to it, see
-tests/test_oracle_golden.py) on a bounded sample of the same workload: the
-first lambdas of the same path, as many as fit the time budget.
+tests/test_oracle_golden.py) on the same workload: complete paths, as many as
+fit its time budget (the line reports how many ran).
+
+After the timed steps rank 0 checks the benchmarked path against the oracle
+on its first lambdas (``parity`` block: epochs, per-checkpoint active sets,
+supports, beta, gaps) and exits non-zero on a mismatch.
 """
 
 from __future__ import annotations
@@ -107,30 +111,15 @@ def _grid(lmax, case):
     return lambda_grid(lmax, case.n_lambdas, case.delta)
 
 
-def _full_path_scale(config: str, k: int):
-    """Scale factor from the first k lambdas to the whole path, from the
-    per-lambda times of one complete CPU path of the same workload measured
-    with the same oracle (profiles/r01/cpu_oracle_<config>_full.json).  The
-    late lambdas dominate (cfg1: the first 64 are 5% of the path), so the
-    bounded sample is scaled to the metric's unit with the measured cost
-    profile, not linearly."""
-    path = os.path.join(ROOT, "profiles", "r01", f"cpu_oracle_{config}_full.json")
-    try:
-        with open(path) as f:
-            per = json.load(f)["per_lambda_s"]
-    except Exception:
-        return None, None
-    if k <= 0 or k > len(per) or sum(per[:k]) <= 0:
-        return None, None
-    return sum(per) / sum(per[:k]), os.path.relpath(path, ROOT)
-
-
-def _roofline_traffic():
+def _roofline_traffic(config: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the screening
-    kernel from the committed ncu --set full capture (profiles/r01)."""
+    kernel, from the NEWEST committed ``ncu --set full`` capture of this config
+    (profiles/r*/ncu_screen_full_<config>*.md, by round then file time)."""
+    import glob
     import re
-    for name in ("ncu_screen_full_cfg1_r01b.md", "ncu_screen_full_cfg1.md"):
-        path = os.path.join(ROOT, "profiles", "r01", name)
+    cands = glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_screen_full_{config}*.md"))
+    cands.sort(key=lambda p: (os.path.basename(os.path.dirname(p)), os.path.getmtime(p)), reverse=True)
+    for path in cands:
         try:
             txt = open(path).read()
         except OSError:
@@ -143,56 +132,103 @@ def _roofline_traffic():
                 if mult:
                     vals[key] = float(m.group(1)) * mult
         if len(vals) == 2:
-            return sum(vals.values()), name
+            return sum(vals.values()), os.path.relpath(path, ROOT)
     return None, None
 
 
-def _cpu_sample(case, grid, budget_s):
+def _parity_mod():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_bench_parity", os.path.join(ROOT, "tests", "parity.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _cpu_sample(case, grid, budget_s, track=False):
     """Oracle (reference algorithm, CPU) on the first lambdas of the same path,
-    stopping after the point at which the budget is exceeded."""
+    stopping after the point at which the budget is exceeded (budget None:
+    the whole path)."""
     from oracle import gapsafe_oracle as O
     X = O.DesignMatrix(case.X)
     t0 = time.perf_counter()
-    res = O.run_path(X, case.y, grid, O.SolverConfig(epsilon=case.epsilon, max_passes=100_000),
+    res = O.run_path(X, case.y, grid, O.SolverConfig(epsilon=case.epsilon, max_passes=100_000,
+                                                     track_active=track),
                      cache_lambda_max=True, time_budget_s=budget_s)
     wall = time.perf_counter() - t0
     return res, wall
 
 
+def _workload_config(args, case, grid):
+    """The ``config`` object, identical in both arms."""
+    n, p = case.X.shape
+    es = case.X.dtype.itemsize
+    return {"workload": args.config, "n": int(n), "p": int(p), "lambdas": int(grid.size), "tol": case.tol,
+            "screen_every": 10, "rule": "gap_sphere",
+            "l2": f"design {n * p * es / 1e6:.0f} MB > 126 MB L2: streamed inputs, no flush needed"}
+
+
 def run_reference(args):
+    """The reference algorithm's CPU implementation (the oracle port, pinned
+    bit-for-bit to the reference's golden paths) on the SAME workload: every
+    timed step is one complete path over all the grid's lambdas.  Steps are
+    run while the time budget allows (at least one), and the line reports the
+    number actually run; the warm-up steps are the path's first lambdas (BLAS
+    threads and the C kernels warm), stated in ``warmup_note``."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
     case = _make_case(args.config)
     from oracle import gapsafe_oracle as O
+    O.build_kernels()
     Xo = O.DesignMatrix(case.X)
     lmax, _ = Xo.max_abs_correlation(case.y)
     grid = O.lambda_grid(lmax, case.n_lambdas, case.delta)
     cores = len(os.sched_getaffinity(0))
-    times, npts = [], None
-    for step in range(args.warmup + args.steps):
-        res, wall = _cpu_sample(case, grid if npts is None else grid[:npts], args.cpu_budget)
-        if npts is None:
-            npts = len(res.timings)
-        if step >= args.warmup:
-            times.append(sum(res.timings))
-    measured = statistics.median(times)
-    scale, src = _full_path_scale(args.config, npts)
-    value = measured * scale if scale else measured
-    sample = (f"first {npts} of {grid.size} lambdas of the {args.config} path (run_path timing scope, path.py:78,94)"
-              + (f", scaled to the whole path x{scale:.3f} by the measured per-lambda cost profile ({src})"
-                 if scale else " (not scaled: no full-path profile)"))
+    for _ in range(args.warmup):
+        O.run_path(Xo, case.y, grid, O.SolverConfig(epsilon=case.epsilon, max_passes=100_000),
+                   cache_lambda_max=True, max_points=3)
+    times, t_all = [], time.perf_counter()
+    while True:
+        res, _ = _cpu_sample(case, grid, None)
+        times.append(sum(res.timings))
+        if len(times) >= args.steps:
+            break
+        spent = time.perf_counter() - t_all
+        if spent + max(times) > args.ref_budget:
+            break
+    value = statistics.mean(times)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+            "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
+            "warmup_note": "each warm-up step is the first 3 lambdas of the same path",
+            "ms_per_step": value * 1e3, "step_s": times,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded, SURVEY.md §8(d))",
-            "config": {"workload": args.config, "n": int(case.X.shape[0]), "p": int(case.X.shape[1]),
-                       "lambdas": int(grid.size), "sample_lambdas": npts, "tol": case.tol},
+            "data": "synthetic (seeded generator, SURVEY.md §8(d))",
+            "config": _workload_config(args, case, grid),
             "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
-                             "sample": sample, "measured_sample_s": measured},
+                             "sample": f"complete {args.config} path ({grid.size} lambdas, run_path timing scope "
+                                       f"path.py:78,94); OpenBLAS on {cores} threads, CD kernels single-threaded "
+                                       f"as in the reference",
+                             "epochs": int(sum(s.passes_done for s in res.states))},
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _gpu_parity(case, grid, cfg_cls, X, dev, k_budget_s, ynsq):
+    """Parity of the benchmarked path against the oracle on its first
+    lambdas: the oracle runs the path with per-checkpoint active sets tracked
+    until ``k_budget_s`` is spent (k lambdas); the device re-runs the same k
+    lambdas with tracking.  Epochs, per-checkpoint active sets (element by
+    element), supports, beta (1e-8 rel) and gaps (D7 floor) are compared."""
+    import paper_1505_03410_b200 as gs
+    ref, wall = _cpu_sample(case, grid, k_budget_s, track=True)
+    k = len(ref.states)
+    cfg = gs.SolverConfig(epsilon=case.epsilon, max_passes=100_000, track_active=True)
+    mine = gs.run_path(X, case.y, grid[:k], cfg, solver=dev)
+    rep = _parity_mod().path_report(mine, ref, ynsq)
+    rep["oracle_s"] = sum(ref.timings)
+    rep["gpu_s"] = sum(mine.timings)
+    return rep, ref
 
 
 def run_ours(args):
@@ -240,6 +276,8 @@ def run_ours(args):
         from paper_1505_03410_b200.dist import max_over_ranks
         ms_step = max_over_ranks(ms_step)
     res = results[-1]
+    # every timed step must produce the same path (determinism)
+    same = all(all(a.passes_done == b.passes_done for a, b in zip(r.states, res.states)) for r in results)
     st = [s.stats for s in res.states]
     agg = {k: sum(x[k] for x in st) for k in ("cd_visits", "cd_uncertified", "cd_nonzero", "checkpoints",
                                              "screen_ms", "ckpt_ms", "refresh_ms", "cd_ms", "n_screen",
@@ -248,13 +286,17 @@ def run_ours(args):
 
     # ---- screening-pass roofline: the fused full-p GEMV + sphere test + compaction
     peak, peak_kind = _peaks()
-    es = 8 if case.X.dtype == np.float64 else 4
-    scr_bytes = n * p * es + p * (8 + 1) + n * 8       # X, norms in, keep marks out, center
+    es = case.X.dtype.itemsize
+    if getattr(X, "is_sparse", False):
+        nnz = int(case.X.nnz)
+        scr_bytes = nnz * (8 + 4) + 8 * (p + 1) + p * (8 + 1) + n * 8
+    else:
+        scr_bytes = n * p * es + p * (8 + 1) + n * 8       # X, norms in, keep marks out, center
     # average launch duration of back-to-back launches (CUDA events on the
     # launching stream); median over 3 batches of 20 to damp run-to-run noise
     scr_ms = statistics.median(timer.screen_pass_ms(X, res.states[-1].theta.theta, 1e-3, reps=20) for _ in range(3))
     achieved = scr_bytes / (scr_ms * 1e-3) / 1e9
-    traffic, traffic_src = _roofline_traffic() if args.config == "cfg1" else (None, None)
+    traffic, traffic_src = _roofline_traffic(args.config)
     inpath_screen = agg["screen_ms"] / max(1, agg["n_screen"])
 
     # ---- e2e through the public API from pinned host buffers
@@ -265,9 +307,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY.md §8(d))",
-        "config": {"workload": args.config, "n": int(n), "p": int(p), "lambdas": int(grid.size),
-                   "tol": case.tol, "screen_every": 10, "parallelism": "replicas" if ws > 1 else "single",
-                   "l2": f"design {n * p * es / 1e6:.0f} MB > 126 MB L2: streamed inputs, no flush needed"},
+        "config": _workload_config(args, case, grid),
+        "parallelism": "replicas" if ws > 1 else "single",
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_screen_full (group_gemv G_MU: full-p screening GEMV + sphere test)",
@@ -277,24 +318,27 @@ def run_ours(args):
                      "in_path_screen_ms": inpath_screen},
         "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "path": {"epochs": epochs, "checkpoints": agg["checkpoints"], "converged": int(res.converged.sum()),
+                 "steps_identical": bool(same),
                  "cd_visits": agg["cd_visits"], "cd_uncertified": agg["cd_uncertified"],
                  "cd_nonzero": agg["cd_nonzero"], "refreshes": agg["n_refresh"],
                  "phase_ms": {"screen": agg["screen_ms"], "checkpoint": agg["ckpt_ms"],
                               "refresh": agg["refresh_ms"], "cd": agg["cd_ms"]},
                  "cd_updates_per_s": agg["cd_uncertified"] / max(1e-9, agg["cd_ms"] * 1e-3)},
     }
+    ok = True
     if rank == 0 and ws == 1 and not args.no_cpu:
-        sample, wall = _cpu_sample(case, grid, args.cpu_budget)
-        k = len(sample.timings)
+        ynsq = float(case.y @ case.y)
+        par, ref = _gpu_parity(case, grid, None, X, dev, args.cpu_budget, ynsq)
+        line["parity"] = par
+        ok = bool(par["ok"])
+        k = par["lambdas_compared"]
         gpu_same = sum(res.timings[:k])
-        measured = sum(sample.timings)
-        scale, src = _full_path_scale(args.config, k)
-        line["cpu_baseline"] = {"value": measured * scale if scale else measured, "unit": "s",
-                                "cores": len(os.sched_getaffinity(0)), "kind": "port",
-                                "sample": (f"first {k} of {grid.size} lambdas of the {args.config} path"
-                                           + (f", scaled to the whole path x{scale:.3f} by the measured per-lambda "
-                                              f"cost profile ({src})" if scale else " (not scaled)")),
-                                "measured_sample_s": measured,
+        measured = sum(ref.timings)
+        line["cpu_baseline"] = {"value": measured, "unit": "s", "cores": len(os.sched_getaffinity(0)),
+                                "kind": "port",
+                                "sample": (f"first {k} of {grid.size} lambdas of the {args.config} path (oracle, "
+                                           f"run_path timing scope path.py:78,94; not scaled); the complete path "
+                                           f"is timed by the reference arm (bench.py --impl reference)"),
                                 "gpu_same_sample_s": gpu_same,
                                 "speedup_same_sample": measured / max(gpu_same, 1e-12)}
     if rank == 0:
@@ -302,7 +346,23 @@ def run_ours(args):
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if not ok:
+        print("bench: PARITY FAILURE against the oracle: " + str(line["parity"].get("first_mismatch")),
+              file=sys.stderr, flush=True)
+        return 3
     return 0
+
+
+def _spawn_ranks(args) -> int:
+    """``--gpus N`` outside torchrun: relaunch this script as N ranks on one
+    node (one process per GPU), the way the driver does."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -313,10 +373,14 @@ def main():
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=900.0,
+                    help="reference arm: stop starting new full paths after this many seconds")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

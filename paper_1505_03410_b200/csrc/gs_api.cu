@@ -225,7 +225,8 @@ extern "C" int gs_matrix_csc(const double* data, const int32_t* indices, const i
 }
 
 extern "C" int gs_matrix_norms_sq(const gs_matrix* M, double* out) {
-    CK(cudaMemcpy(out, M->norms_sq, M->p * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(out, M->norms_sq, M->p * 8, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaStreamSynchronize(M->st));
     return GS_OK;
 }
 
@@ -404,7 +405,8 @@ extern "C" int gs_matvec(const gs_matrix* M, const double* beta, double* out) {
     TRY(tb.get(&db, M->p)); TRY(tb.get(&dout, M->n));
     CK(cudaMemcpyAsync(db, beta, M->p * 8, cudaMemcpyHostToDevice, st));
     TRY(matvec_dev(M, st, tb, db, nullptr, dout));
-    CK(cudaMemcpy(out, dout, M->n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(out, dout, M->n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     return GS_OK;
 }
 
@@ -915,13 +917,22 @@ extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* 
 
     // ---- the persistent solve
     if (active0_mode == 1) {
-        std::vector<int32_t> c32(std::max<int64_t>(n0, 1));
+        // the device marks the listed columns (the active set is their
+        // ascending, duplicate-free compaction), so a list is deduplicated
+        // here: at most p entries reach S->A2 (p slots)
+        std::vector<char> seen((size_t)p, 0);
+        std::vector<int32_t> c32;
+        c32.reserve((size_t)std::min<int64_t>(std::max<int64_t>(n0, 1), p));
         for (int64_t i = 0; i < n0; ++i) {
             if (active0[i] < 0 || active0[i] >= p) return fail(GS_ERR_INDEX, "active0 index out of range");
-            c32[i] = (int32_t)active0[i];
+            if (!seen[(size_t)active0[i]]) { seen[(size_t)active0[i]] = 1; c32.push_back((int32_t)active0[i]); }
         }
-        if (n0) CK(cudaMemcpyAsync(S->A2, c32.data(), n0 * 4, cudaMemcpyHostToDevice, st));
-        h->cnt = n0;
+        const int64_t nu = (int64_t)c32.size();
+        if (nu) {
+            CK(cudaMemcpyAsync(S->A2, c32.data(), nu * 4, cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));   // c32 is a host temporary
+        }
+        h->cnt = nu;
     }
     TRY(sc_upload(S));
     memset(S->hctl, 0, sizeof(SolveCtl));
@@ -1141,7 +1152,8 @@ extern "C" int gs_screen_timed(const gs_matrix* M, const double* center, double 
         float f = 0.0f;
         cudaEventElapsedTime(&f, e0, e1);
         *ms = f / reps;
-        CK(cudaMemcpy(n_active, cnt, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(n_active, cnt, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
     }
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     s.release();

@@ -1,6 +1,7 @@
-// Launchers of the persistent solver kernels, one translation unit per
-// storage type (gs_solve_f64.cu, gs_solve_f32.cu) so the heavy template
-// instantiations compile in parallel.  Every function returns a cudaError_t.
+// Launchers of the persistent solver kernels: one translation unit per
+// (storage type, rows per lane) -- gs_solve_inst.cu compiled with -D flags --
+// so the heavy template instantiations compile in parallel; gs_launch.cu
+// dispatches on R.  Every function returns a cudaError_t.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstddef>
@@ -10,7 +11,14 @@ struct SolveDev;
 struct BatchOut;
 }  // namespace gs
 
+#define GS_DECLARE_R(SUF, R)                                                                                  \
+    cudaError_t gs_launch_solve_##SUF##_r##R(cudaStream_t st, const gs::SolveDev* dprobs, int G, int nprob,          \
+                                             size_t smem);                                                        \
+    cudaError_t gs_launch_cdpass_##SUF##_r##R(cudaStream_t st, const gs::SolveDev* dprobs, size_t smem);             \
+    cudaError_t gs_launch_batch_##SUF##_r##R(cudaStream_t st, gs::SolveDev* dprobs, const gs::BatchOut* douts,       \
+                                             int B, size_t smem);
 #define GS_DECLARE_LAUNCHERS(SUF)                                                                              \
+    GS_DECLARE_R(SUF, 1) GS_DECLARE_R(SUF, 2) GS_DECLARE_R(SUF, 4) GS_DECLARE_R(SUF, 8) GS_DECLARE_R(SUF, 48)    \
     cudaError_t gs_launch_solve_##SUF(int R, cudaStream_t st, const gs::SolveDev* dprobs, int G, int nprob,        \
                                       size_t smem);                                                            \
     cudaError_t gs_launch_cdpass_##SUF(int R, cudaStream_t st, const gs::SolveDev* dprobs, size_t smem);           \
@@ -22,3 +30,4 @@ struct BatchOut;
 GS_DECLARE_LAUNCHERS(f64)
 GS_DECLARE_LAUNCHERS(f32)
 #undef GS_DECLARE_LAUNCHERS
+#undef GS_DECLARE_R

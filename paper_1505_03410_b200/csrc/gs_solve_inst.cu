@@ -1,5 +1,8 @@
-// Instantiates the persistent solver kernels for storage type GS_T and
-// defines the gs_launch_*_<GS_SUF> launchers declared in gs_launch.h.
+// Instantiates the persistent solver kernels for storage type GS_T and rows
+// per lane GS_R, and defines the gs_launch_*_<GS_SUF>_r<GS_R> launchers
+// declared in gs_launch.h.  build() compiles this file once per (type, R)
+// with -DGS_T=... -DGS_SUF=... -DGS_R=..., so the heavy instantiations build
+// in parallel; gs_launch.cu dispatches on R at run time.
 #include "gs_launch.h"
 #include "gs_solve.cuh"
 
@@ -7,6 +10,7 @@ using namespace gs;
 
 #define GS_CAT2(a, b) a##b
 #define GS_CAT(a, b) GS_CAT2(a, b)
+#define GS_NAME(base) GS_CAT(GS_CAT(GS_CAT(base, GS_SUF), _r), GS_R)
 
 namespace {
 constexpr int kThreads = 256;
@@ -50,38 +54,24 @@ cudaError_t batch_R(cudaStream_t st, SolveDev* dprobs, const BatchOut* douts, in
 }
 }  // namespace
 
-cudaError_t GS_CAT(gs_launch_solve_, GS_SUF)(int R, cudaStream_t st, const SolveDev* dprobs, int G, int nprob,
-                                             size_t smem) {
-    switch (R) {
-        case 1: return solve_R<1>(st, dprobs, G, nprob, smem);
-        case 2: return solve_R<2>(st, dprobs, G, nprob, smem);
-        case 4: return solve_R<4>(st, dprobs, G, nprob, smem);
-        case 8: return solve_R<8>(st, dprobs, G, nprob, smem);
-        default: return solve_R<48>(st, dprobs, G, nprob, smem);
-    }
+cudaError_t GS_NAME(gs_launch_solve_)(cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem) {
+    return solve_R<GS_R>(st, dprobs, G, nprob, smem);
 }
 
-cudaError_t GS_CAT(gs_launch_cdpass_, GS_SUF)(int R, cudaStream_t st, const SolveDev* dprobs, size_t smem) {
-    switch (R) {
-        case 1: return cdpass_R<1>(st, dprobs, smem);
-        case 2: return cdpass_R<2>(st, dprobs, smem);
-        case 4: return cdpass_R<4>(st, dprobs, smem);
-        case 8: return cdpass_R<8>(st, dprobs, smem);
-        default: return cdpass_R<48>(st, dprobs, smem);
-    }
+cudaError_t GS_NAME(gs_launch_cdpass_)(cudaStream_t st, const SolveDev* dprobs, size_t smem) {
+    return cdpass_R<GS_R>(st, dprobs, smem);
 }
 
-cudaError_t GS_CAT(gs_launch_batch_, GS_SUF)(int R, cudaStream_t st, SolveDev* dprobs, const BatchOut* douts, int B,
-                                             size_t smem) {
-    switch (R) {
-        case 1: return batch_R<1>(st, dprobs, douts, B, smem);
-        case 2: return batch_R<2>(st, dprobs, douts, B, smem);
-        case 4: return batch_R<4>(st, dprobs, douts, B, smem);
-        case 8: return batch_R<8>(st, dprobs, douts, B, smem);
-        default: return cudaErrorInvalidValue;     // batched problems: n <= 1792
-    }
+cudaError_t GS_NAME(gs_launch_batch_)(cudaStream_t st, SolveDev* dprobs, const BatchOut* douts, int B, size_t smem) {
+#if GS_R <= 8
+    return batch_R<GS_R>(st, dprobs, douts, B, smem);
+#else
+    (void)st; (void)dprobs; (void)douts; (void)B; (void)smem;
+    return cudaErrorInvalidValue;     // batched problems: n <= 1792
+#endif
 }
 
+#if GS_R == 1
 cudaError_t GS_CAT(gs_launch_screen_full_, GS_SUF)(cudaStream_t st, const SolveDev* dprobs, double radius, int grid,
                                                    size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(k_screen_full<GS_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -89,3 +79,4 @@ cudaError_t GS_CAT(gs_launch_screen_full_, GS_SUF)(cudaStream_t st, const SolveD
     k_screen_full<GS_T><<<(unsigned)grid, kThreads, smem, st>>>(dprobs, radius);
     return cudaGetLastError();
 }
+#endif

@@ -170,7 +170,7 @@ class DeviceSolver:
         if config.rule not in _GPU_RULES:
             raise NotImplementedError(
                 f"rule {config.rule.value!r} is not on the B200 path in this build "
-                f"(supported: none, gap_sphere; SURVEY.md §8(f))")
+                f"(supported: {', '.join(r.value for r in _GPU_RULES)})")
         X = self.X
         n, p = X.n_rows, X.n_cols
         cap = config.max_passes // config.screen_every + 4
@@ -245,9 +245,17 @@ def solve(prob: LassoProblem, config: SolverConfig, warm_beta: np.ndarray | None
     if config.rule not in _GPU_RULES:
         raise NotImplementedError(
             f"rule {config.rule.value!r} is not on the B200 path in this build "
-            f"(supported: none, gap_sphere; SURVEY.md §8(f))")
+            f"(supported: {', '.join(r.value for r in _GPU_RULES)})")
     if prob.lam > prob.lambda_max * (1 + 1e-12):
         raise ValueError(f"lambda={prob.lam} exceeds lambda_max={prob.lambda_max}")
+    if active0 is not None:
+        a0 = np.asarray(active0, dtype=np.int64).ravel()
+        if a0.size > 1 and not np.all(a0[1:] > a0[:-1]):
+            # the reference visits active0 in the given order, duplicates
+            # included (solver.py:171-174); the device CD visits an ascending,
+            # duplicate-free active set, so any other order is refused loudly
+            raise NotImplementedError("active0 must be strictly ascending on the B200 path "
+                                      "(as a screen's active_set is)")
     dev = _solver_for(prob)
     dev.set_beta(warm_beta)
     if active0 is None:

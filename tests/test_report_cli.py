@@ -12,18 +12,8 @@ from paper_1505_03410_b200 import report
 from paper_1505_03410_b200.cli import build_parser, config_from_args
 
 
-def _write_dense_csv(path, X, y):
-    with open(path, "w", encoding="utf-8", newline="\n") as fh:
-        fh.write(",".join(["y"] + [f"f{j + 1}" for j in range(X.shape[1])]) + "\n")
-        for i in range(X.shape[0]):
-            fh.write(",".join([repr(float(y[i]))] + [repr(float(v)) for v in X[i]]) + "\n")
-
-
-def _write_svmlight(path, X, y):
-    with open(path, "w", encoding="utf-8", newline="\n") as fh:
-        for i in range(X.shape[0]):
-            nz = np.flatnonzero(X[i])
-            fh.write(" ".join([repr(float(y[i]))] + [f"{j + 1}:{float(X[i, j])!r}" for j in nz]) + "\n")
+def _write_npz(path, X, y):
+    np.savez(path, X=X, y=y)
 
 
 def _data(n=25, p=40, seed=11):
@@ -50,31 +40,11 @@ class TestRunConfig:
 
 
 def test_cli_parses_reference_arguments(tmp_path):
-    args = build_parser().parse_args(["bench", "--data", "x.csv", "--rules", "none, gap_dome",
+    args = build_parser().parse_args(["bench", "--data", "x.npz", "--rules", "none, gap_dome",
                                       "--eps", "1e-4,1e-6", "--grid-T", "7", "--out", str(tmp_path)])
     cfg = config_from_args(args)
     assert [r.value for r in cfg.rules] == ["none", "gap_dome"]
     assert cfg.epsilons == [1e-4, 1e-6] and cfg.grid_T == 7 and cfg.grid_delta == 3.0
-
-
-@pytest.mark.parametrize("fmt", ["dense-csv", "svmlight"])
-def test_dataset_formats_round_trip(tmp_path, fmt):
-    X, y = _data()
-    path = tmp_path / ("d.csv" if fmt == "dense-csv" else "d.svm")
-    (_write_dense_csv if fmt == "dense-csv" else _write_svmlight)(path, X, y)
-    A, yy = report.parse_dataset(path, fmt)
-    A = A.toarray() if hasattr(A, "toarray") else A
-    assert np.array_equal(A, X) and np.array_equal(yy, y)
-
-
-def test_dataset_format_errors(tmp_path):
-    bad = tmp_path / "b.svm"
-    bad.write_text("1.0 0:3.0\n")
-    with pytest.raises(report.DatasetFormatError):
-        report.parse_dataset(bad, "svmlight")
-    bad.write_text("y,f1\n1.0,2.0,3.0\n")
-    with pytest.raises(report.DatasetFormatError):
-        report.parse_dataset(bad, "dense-csv")
 
 
 @pytest.mark.gpu
@@ -109,8 +79,8 @@ def test_reports_match_reference_schemas(tmp_path):
 def test_cli_bench_end_to_end(tmp_path, capsys):
     from paper_1505_03410_b200.cli import main
     X, y = _data()
-    path = tmp_path / "d.csv"
-    _write_dense_csv(path, X, y)
+    path = tmp_path / "d.npz"
+    _write_npz(path, X, y)
     assert main(["bench", "--data", str(path), "--rules", "none,gap_sphere,static", "--grid-T", "4",
                  "--out", str(tmp_path / "o")]) == 0
     assert "converged=4/4" in capsys.readouterr().out
