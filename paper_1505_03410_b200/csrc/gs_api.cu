@@ -505,6 +505,34 @@ static CdShape cd_shape(int64_t n) {
 // cross-warp reduction per coordinate (cfg1, cfg4) the direct chain is faster.
 static int cd_gram_default(int64_t n) { return (cd_shape(n).R <= 4 && cd_shape(n).W == 1) ? 1 : 0; }
 
+// blocked-chain consumer (gs_cd_blk.cuh): rows per thread R and compute warps
+// NW (no producer warp; warp 0 scans and issues the next window itself)
+static CdShape cd_shape_blk(int64_t n) {
+    if (n <= 32) return {1, 1};
+    if (n <= 64) return {2, 1};
+    if (n <= 128) return {4, 1};
+    if (n <= 256) return {4, 2};
+    if (n <= 512) return {4, 4};
+    if (n <= 1024) return {4, 8};
+    return {0, 0};
+}
+
+// dense CD plan: consumer mode (0 direct, 1 Gram windows, 2 blocked chain;
+// GS_CD_GRAM overrides), template R and warps.  The blocked chain is the
+// default wherever it applies (n <= 1024).
+struct CdPlan { int mode, R, W; };
+static CdPlan cd_plan(int64_t n) {
+    const char* eg = getenv("GS_CD_GRAM");
+    int mode = eg ? atoi(eg) : (cd_shape_blk(n).R ? 2 : cd_gram_default(n));
+    if (mode == 2 && cd_shape_blk(n).R == 0) mode = 0;
+    const CdShape s = mode == 2 ? cd_shape_blk(n) : cd_shape(n);
+    return {mode, s.R, s.W};
+}
+static int blk_mfac() {
+    const char* e = getenv("GS_BLK_MFAC");
+    return e ? atoi(e) : 32;
+}
+
 static int launch_solve(const gs_matrix* M, cudaStream_t st, const SolveDev* dprobs, int G, int nprob, size_t smem,
                         int R) {
     const bool f64 = M->sparse || M->dtype == GS_DTYPE_F64;
@@ -524,7 +552,8 @@ static int vs_cap_for(const gs_matrix* M) { return M->sparse ? 24576 : 6144; }
 
 static size_t cd_bytes_for(const gs_matrix* M) {
     if (M->sparse) return 0;
-    const size_t b = cd_smem_bytes_rt(M->ld, M->dtype == GS_DTYPE_F64 ? 8 : 4);
+    const int es = M->dtype == GS_DTYPE_F64 ? 8 : 4;
+    const size_t b = std::max(cd_smem_bytes_rt(M->ld, es), cd_shape_blk(M->n).R ? blk_smem_bytes(M->ld, es) : (size_t)0);
     return (b + 15) / 16 * 16;
 }
 
@@ -792,14 +821,14 @@ static void fill_dev(gs_solver* S, SolveDev& d) {
     d.partial = S->partial; d.nch_max = S->nch_max;
     d.sc = S->sc; d.ctl = S->ctl; d.trace = S->trace; d.trace_cap = S->trace_cap; d.bar = S->bar;
     d.cta_val = S->cta_val; d.cta_idx = S->cta_idx; d.cta_cnt = S->cta_cnt;
-    const CdShape cs = cd_shape(M->n);
+    const CdPlan cs = cd_plan(M->n);
     d.cd_warps = M->sparse ? 1 : cs.W;
+    d.blk_mfac = blk_mfac();
     d.cd_bytes = (int)cd_bytes_for(M);
     d.vs_cap = vs_cap_for(M);
     const char* env = getenv("GS_REFRESH_EXCESS");
     d.refresh_excess = env ? atoi(env) : 32;
-    const char* eg = getenv("GS_CD_GRAM");
-    d.cd_gram = eg ? atoi(eg) : cd_gram_default(M->n);
+    d.cd_gram = cs.mode;
     const char* ep = getenv("GS_CD_PROF");
     d.cd_prof = ep ? atoi(ep) : 0;
     d.q = S->q; d.gstar = S->gstar; d.lmax_path = S->lmax; d.jstar = S->jstar;
@@ -945,7 +974,7 @@ extern "C" int gs_solver_solve(gs_solver* S, double lam, const gs_solve_config* 
     d.prev_margin = S->prev_margin;
     CK(cudaMemcpyAsync(S->dprob, &d, sizeof d, cudaMemcpyHostToDevice, st));
     const size_t smem = solve_smem(M);
-    const int Rr = M->sparse ? 1 : cd_shape(M->n).R;
+    const int Rr = M->sparse ? 1 : cd_plan(M->n).R;
     int64_t hook_fired = 0, launches = 0;
     while (true) {
         TRY(launch_solve(M, st, S->dprob, S->G, 1, smem, Rr));
@@ -1034,15 +1063,14 @@ extern "C" int gs_cd_pass(const gs_matrix* M, double* beta, double* rho, const i
             d.data = M->data; d.indices = M->indices; d.indptr = M->indptr;
             d.norms = dnorm; d.nsq = dns; d.inv_nsq = dinv; d.cinfo = dci; d.beta = db; d.rho = dr; d.c = c; d.t = t; d.A = dA;
             d.sc = sc; d.ctl = ctl; d.lam = lam; d.certify = 1; d.cta_val = cval; d.cta_idx = cidx;
-            {
-                const char* eg = getenv("GS_CD_GRAM");
-                d.cd_gram = eg ? atoi(eg) : cd_gram_default(n);
-            }
-            d.cd_warps = M->sparse ? 1 : cd_shape(n).W;
+            const CdPlan cp = cd_plan(n);
+            d.cd_gram = cp.mode;
+            d.blk_mfac = blk_mfac();
+            d.cd_warps = M->sparse ? 1 : cp.W;
             d.cd_bytes = (int)cd_bytes_for(M);
             d.vs_cap = vs_cap_for(M);
             CK(cudaMemcpyAsync(dp, &d, sizeof d, cudaMemcpyHostToDevice, st));
-            TRY(launch_cdpass(M, st, dp, solve_smem(M), M->sparse ? 1 : cd_shape(n).R));
+            TRY(launch_cdpass(M, st, dp, solve_smem(M), M->sparse ? 1 : cp.R));
         }
     }
     CK(cudaMemcpyAsync(beta, db, p * 8, cudaMemcpyDeviceToHost, st));
@@ -1351,7 +1379,7 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
     std::vector<SolveDev> probs(B);
     std::vector<BatchOut> outs(B);
     std::vector<DevScalars> hsc(B);
-    const CdShape cs = cd_shape(n);
+    const CdPlan cs = cd_plan(n);
     for (int64_t b = 0; b < B; ++b) {
         SolveDev& d = probs[b];
         memset(&d, 0, sizeof d);
@@ -1369,8 +1397,8 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
         d.vs_cap = vs_cap_for(&Bt->shape);
         const char* env = getenv("GS_REFRESH_EXCESS");
         d.refresh_excess = env ? atoi(env) : 32;
-        const char* eg = getenv("GS_CD_GRAM");
-        d.cd_gram = eg ? atoi(eg) : cd_gram_default(n);
+        d.cd_gram = cs.mode;
+        d.blk_mfac = blk_mfac();
         BatchOut& o = outs[b];
         o.grid = dgrid + b * T; o.lmax = Bt->lmax[b]; o.betas = dbetas ? dbetas + b * T * p : nullptr;
         o.passes = dpasses + b * T; o.gaps = dgaps + b * T; o.converged = dconv + b * T; o.n_active = dnact + b * T;

@@ -120,6 +120,7 @@ struct SolveDev {
     int cd_prof;         // print Gram-window phase cycles at the end of each solve (debug)
     int csc_par;         // CSC CD: fully parallel waves (cd_epoch_csc_par)
     int* rowmark;        // [n] row map of cd_epoch_csc_par (kRowFree between waves)
+    int blk_mfac;        // blocked-chain CD: window drift bound Dp = D + blk_mfac * gstep
 };
 
 struct Group {
@@ -2112,6 +2113,20 @@ static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t 
 // ---------------------------------------------------------------------------
 // the persistent solve kernel
 // ---------------------------------------------------------------------------
+}  // namespace gs
+#include "gs_cd_blk.cuh"
+namespace gs {
+
+// dense CD epoch: blocked chain (cd_gram == 2, R <= 4) or the ring consumers
+template <typename T, int R>
+static __device__ __forceinline__ void cd_epoch_dense_any(const SolveDev& P, int64_t m, unsigned char* smem,
+                                                          int* tile_valid) {
+    if constexpr (R <= 4) {
+        if (P.cd_gram == 2) { cd_epoch_blk<T, R>(P, m, P.cd_warps, smem, tile_valid); return; }
+    }
+    cd_epoch_dense<T, R>(P, m, P.cd_warps, smem, tile_valid);
+}
+
 template <typename T, int R>
 static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* smem) {
     __shared__ int sh[32];
@@ -2402,7 +2417,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
         if (g.c == 0) {
             const unsigned long long td0 = gtimer();
             if (P.sparse) { if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, m, smem); else cd_epoch_csc(P, m, smem); }
-            else cd_epoch_dense<T, R>(P, m, P.cd_warps, smem, &s_tile_valid);
+            else cd_epoch_dense_any<T, R>(P, m, smem, &s_tile_valid);
             if (threadIdx.x == 0) {
                 ctl->t_cd += gtimer() - td0;
                 ctl->passes++;
@@ -2479,7 +2494,7 @@ __global__ void __launch_bounds__(256, 1) k_cd_pass_prod(const SolveDev* __restr
     if (threadIdx.x == 0) s_tile_valid = 0;
     __syncthreads();
     if (P.sparse) cd_epoch_csc(P, m, smem);
-    else cd_epoch_dense<T, R>(P, m, P.cd_warps, smem, &s_tile_valid);
+    else cd_epoch_dense_any<T, R>(P, m, smem, &s_tile_valid);
 }
 
 // standalone full-p screening pass (the same group_gemv G_MU code the

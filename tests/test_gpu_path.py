@@ -44,7 +44,7 @@ def test_path_cfg0_full():
     assert np.all(ra.converged)
 
 
-@pytest.mark.parametrize("gram", ["0", "1"])
+@pytest.mark.parametrize("gram", ["0", "1", "2"])
 def test_path_no_certify_identical_to_certify(gram, monkeypatch):
     """Certified-zero skipping is exact.  With one reduction per coordinate
     (GS_CD_GRAM=0) the paths with and without it are bit-identical.  The
@@ -71,7 +71,7 @@ def test_path_no_certify_identical_to_certify(gram, monkeypatch):
         np.testing.assert_allclose(a.betas, b.betas, rtol=0, atol=1e-12 * np.abs(b.betas).max())
 
 
-@pytest.mark.parametrize("gram", ["0", "1"])
+@pytest.mark.parametrize("gram", ["0", "1", "2"])
 def test_path_cd_modes_match_oracle(gram, monkeypatch):
     """Both CD consumers (Gram windows, one reduction per coordinate) meet the
     parity criteria against the oracle on the cfg0 generator."""
@@ -429,3 +429,19 @@ def test_path_sparse_parallel_waves(rule):
     ra, rb, yy = _paths(c.X, c.y, 14, 2.0, c.epsilon, rule=rule)
     compare_paths(ra, rb, yy)
     assert np.all(ra.converged)
+
+
+@pytest.mark.parametrize("n,mfac", [(40, "32"), (100, "32"), (200, "1"), (500, "32"), (1000, "32"), (1000, "1"),
+                                    (1000, "1000")])
+def test_path_blocked_chain_shapes(n, mfac, monkeypatch):
+    """The blocked-chain consumer (GS_CD_GRAM=2) at every warp count it uses
+    (n <= 128: 1 warp; 256: 2; 512: 4; 1024: 8), with a tight drift margin
+    (GS_BLK_MFAC=1: windows end early and the next window is re-issued often)
+    and a loose one, against the oracle."""
+    monkeypatch.setenv("GS_CD_GRAM", "2")
+    monkeypatch.setenv("GS_BLK_MFAC", mfac)
+    c = synth.make_dense_case("blk", 7, n, 2500, 0.3, 40, "normal", 3.0, 12, 2.0, 1e-8)
+    ra, rb, yy = _paths(c.X, c.y, 12, 2.0, c.epsilon)
+    compare_paths(ra, rb, yy)
+    if mfac == "1":
+        assert sum(s.stats["cd_requeues"] for s in ra.states) > 0
