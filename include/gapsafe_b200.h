@@ -164,9 +164,13 @@ typedef struct gs_batch gs_batch;
 int gs_batch_create(const gs_matrix *X0, const double *y0, const int32_t *rows, int64_t B, int64_t n,
                     gs_batch **out);
 int gs_batch_lambda_max(gs_batch *Bt, double *lambda_max);      /* [B] */
-/* grids: [B*T] (each non-increasing).  Outputs [B*T] (betas [B*T*p], may be NULL). */
-int gs_batch_run_paths(gs_batch *Bt, const double *grids, int64_t T, const gs_solve_config *cfg, double *betas,
-                       int64_t *passes, double *gaps, int32_t *converged, int64_t *n_active, double *device_ms);
+/* grids: [B*T] (each non-increasing).  eps: per-problem gap tolerances [B]
+ * (the reference takes epsilon per solve, solver.py:37,226; configs[4] uses
+ * 1e-8 ||y_b||^2), or NULL for cfg->epsilon everywhere.  Outputs [B*T] (betas
+ * [B*T*p], may be NULL). */
+int gs_batch_run_paths(gs_batch *Bt, const double *grids, int64_t T, const gs_solve_config *cfg, const double *eps,
+                       double *betas, int64_t *passes, double *gaps, int32_t *converged, int64_t *n_active,
+                       double *device_ms);
 void gs_batch_free(gs_batch *Bt);
 
 /* ---- measurement support ---------------------------------------------------- */
@@ -178,7 +182,7 @@ int gs_solver_timer(gs_solver *S, int op, double *ms);
  * the matrix stream and timed with CUDA events; *ms is the average per launch,
  * *n_active the survivors. */
 int gs_screen_timed(const gs_matrix *M, const double *center, double radius, int reps, double *ms,
-                    int64_t *n_active);
+                    int64_t *n_active, int32_t *active_out /* [p] or NULL: the survivors, ascending */);
 /* pinned (page-locked) host memory for H2D/D2H at full PCIe rate */
 int gs_host_alloc(int64_t bytes, void **out);
 void gs_host_free(void *ptr);

@@ -92,12 +92,12 @@ SIGNATURES = {
                                 ctypes.c_int, ctypes.POINTER(SolveResult)]),
     "gs_solver_free": (None, [c_vp]),
     "gs_solver_timer": (c_i32, [c_vp, ctypes.c_int, P_f64]),
-    "gs_screen_timed": (c_i32, [c_vp, P_f64, c_dbl, ctypes.c_int, P_f64, P_i64]),
+    "gs_screen_timed": (c_i32, [c_vp, P_f64, c_dbl, ctypes.c_int, P_f64, P_i64, P_i32]),
     "gs_host_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
     "gs_host_free": (None, [c_vp]),
     "gs_batch_create": (c_i32, [c_vp, P_f64, P_i32, c_i64, c_i64, ctypes.POINTER(c_vp)]),
     "gs_batch_lambda_max": (c_i32, [c_vp, P_f64]),
-    "gs_batch_run_paths": (c_i32, [c_vp, P_f64, c_i64, ctypes.POINTER(SolveConfig), P_f64, P_i64, P_f64,
+    "gs_batch_run_paths": (c_i32, [c_vp, P_f64, c_i64, ctypes.POINTER(SolveConfig), P_f64, P_f64, P_i64, P_f64,
                                    P_i32, P_i64, P_f64]),
     "gs_batch_free": (None, [c_vp]),
 }

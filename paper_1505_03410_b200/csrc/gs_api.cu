@@ -557,11 +557,44 @@ static size_t cd_bytes_for(const gs_matrix* M) {
     return (b + 15) / 16 * 16;
 }
 
+// GEMV modes per shape (gs_solve.cuh): whole-CTA column reduction for dense
+// columns of 16 KB and more; 8 lanes per column for short CSC columns
+static bool gemv_wide_for(const gs_matrix* M) {
+    if (M->sparse) return false;
+    const char* e = getenv("GS_GEMV_WIDE");
+    if (e) return atoi(e) != 0 && M->n <= 256 * kWideRows;
+    const int64_t colb = M->ld * (M->dtype == GS_DTYPE_F64 ? 8 : 4);
+    return colb >= 16 * 1024 && M->n <= 256 * kWideRows;
+}
+static bool csc_short_for(const gs_matrix* M) {
+    if (!M->sparse) return false;
+    const char* e = getenv("GS_CSC_SHORT");
+    if (e) return atoi(e) != 0;
+    return M->p > 0 && M->nnz <= 24 * M->p;
+}
+
 static size_t solve_smem(const gs_matrix* M) {
     const int64_t n = M->n;
-    const size_t vs = (n <= vs_cap_for(M)) ? (size_t)(n + 2) * 8 : 0;
+    const size_t vs = (n <= vs_cap_for(M) && !gemv_wide_for(M)) ? (size_t)(n + 2) * 8 : 0;
     if (M->sparse) return std::max(vs, cd_csc_smem_bytes(n));
-    return cd_bytes_for(M) + vs;     // dense: CD tile + column ring stay resident beside the GEMV staging
+    size_t b = cd_bytes_for(M) + vs;     // dense: CD tile + column ring stay resident beside the GEMV staging
+    if (gemv_wide_for(M)) {
+        // the column ring of the wide GEMV takes all of it: as many whole columns as fit (up to 8)
+        const size_t colb = (size_t)M->ld * (M->dtype == GS_DTYPE_F64 ? 8 : 4);
+        const size_t cap = 224 * 1024;
+        const size_t want = std::min<size_t>(cap / colb, kWideSlots) * colb;
+        b = std::max(b, want);
+    }
+    return b;
+}
+
+// shared-memory / GEMV plan fields of a SolveDev
+static void set_plan(const gs_matrix* M, SolveDev& d) {
+    d.vs_cap = gemv_wide_for(M) ? 0 : vs_cap_for(M);
+    d.cd_bytes = (int)cd_bytes_for(M);
+    d.gemv_wide = gemv_wide_for(M) ? 1 : 0;
+    d.csc_short = csc_short_for(M) ? 1 : 0;
+    d.smem_total = (int)solve_smem(M);
 }
 
 static int check_shape(const gs_matrix* M) {
@@ -824,8 +857,7 @@ static void fill_dev(gs_solver* S, SolveDev& d) {
     const CdPlan cs = cd_plan(M->n);
     d.cd_warps = M->sparse ? 1 : cs.W;
     d.blk_mfac = blk_mfac();
-    d.cd_bytes = (int)cd_bytes_for(M);
-    d.vs_cap = vs_cap_for(M);
+    set_plan(M, d);
     const char* env = getenv("GS_REFRESH_EXCESS");
     d.refresh_excess = env ? atoi(env) : 32;
     d.cd_gram = cs.mode;
@@ -1067,8 +1099,7 @@ extern "C" int gs_cd_pass(const gs_matrix* M, double* beta, double* rho, const i
             d.cd_gram = cp.mode;
             d.blk_mfac = blk_mfac();
             d.cd_warps = M->sparse ? 1 : cp.W;
-            d.cd_bytes = (int)cd_bytes_for(M);
-            d.vs_cap = vs_cap_for(M);
+            set_plan(M, d);
             CK(cudaMemcpyAsync(dp, &d, sizeof d, cudaMemcpyHostToDevice, st));
             TRY(launch_cdpass(M, st, dp, solve_smem(M), M->sparse ? 1 : cp.R));
         }
@@ -1137,7 +1168,7 @@ extern "C" int gs_solver_timer(gs_solver* S, int op, double* ms) {
 }
 
 extern "C" int gs_screen_timed(const gs_matrix* M, const double* center, double radius, int reps, double* ms,
-                               int64_t* n_active) {
+                               int64_t* n_active, int32_t* active_out) {
     TRY(ensure_device());
     if (reps < 1) reps = 1;
     cudaStream_t st = M->st;
@@ -1151,7 +1182,8 @@ extern "C" int gs_screen_timed(const gs_matrix* M, const double* center, double 
     d.X = M->X; d.ld = M->ld; d.n = (int)M->n; d.dtype = M->dtype; d.p = M->p; d.sparse = M->sparse;
     d.data = M->data; d.indices = M->indices; d.indptr = M->indptr; d.norms = M->norms; d.nsq = M->norms_sq;
     d.inv_nsq = M->inv_nsq;
-    d.theta = dv; d.mark = mark; d.vs_cap = vs_cap_for(M); d.cd_bytes = (int)cd_bytes_for(M);
+    d.theta = dv; d.mark = mark;
+    set_plan(M, d);
     CK(cudaMemcpyAsync(dp, &d, sizeof d, cudaMemcpyHostToDevice, st));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1182,6 +1214,11 @@ extern "C" int gs_screen_timed(const gs_matrix* M, const double* center, double 
         *ms = f / reps;
         CK(cudaMemcpyAsync(n_active, cnt, 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (active_out && *n_active > 0) {
+            // survivors of the warm-up pass (the timed launches recompute the same marks)
+            CK(cudaMemcpyAsync(active_out, out, (size_t)*n_active * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
     }
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     s.release();
@@ -1352,9 +1389,14 @@ extern "C" int gs_batch_lambda_max(gs_batch* Bt, double* lmax) {
 extern "C" void gs_batch_free(gs_batch* Bt) { batch_release(Bt); }
 
 extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, const gs_solve_config* cfg,
-                                  double* betas, int64_t* passes, double* gaps, int32_t* converged,
-                                  int64_t* n_active, double* device_ms) {
-    if (cfg->epsilon <= 0) return fail(GS_ERR_VALUE, "epsilon must be positive");
+                                  const double* eps, double* betas, int64_t* passes, double* gaps,
+                                  int32_t* converged, int64_t* n_active, double* device_ms) {
+    // eps: per-problem gap tolerances [B] (solver.py:37,226 takes epsilon per
+    // solve); NULL runs every problem at cfg->epsilon
+    if (!eps && cfg->epsilon <= 0) return fail(GS_ERR_VALUE, "epsilon must be positive");
+    if (eps)
+        for (int64_t b = 0; b < Bt->B; ++b)
+            if (!(eps[b] > 0)) return fail(GS_ERR_VALUE, "epsilon must be positive");
     if (cfg->screen_every < 1 || cfg->max_passes < 1) return fail(GS_ERR_VALUE, "bad solver configuration");
     if (cfg->on_checkpoint) return fail(GS_ERR_VALUE, "checkpoint hooks are not available in batched mode");
     if (cfg->rule != GS_RULE_NONE && cfg->rule != GS_RULE_GAP_SPHERE)
@@ -1392,9 +1434,9 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
         d.partial = Bt->partial + b * Bt->nch_max * n; d.nch_max = Bt->nch_max;
         d.sc = Bt->sc + b; d.ctl = Bt->ctl + b; d.trace = Bt->trace + b * cap; d.trace_cap = cap;
         d.cta_val = Bt->cta_val + b; d.cta_idx = Bt->cta_idx + b; d.cta_cnt = Bt->cta_cnt + 2 * b;
-        d.eps = cfg->epsilon; d.max_passes = cfg->max_passes; d.f = cfg->screen_every; d.rule = cfg->rule;
-        d.certify = cfg->certify; d.cd_warps = cs.W; d.cd_bytes = (int)cd_bytes_for(&Bt->shape);
-        d.vs_cap = vs_cap_for(&Bt->shape);
+        d.eps = eps ? eps[b] : cfg->epsilon; d.max_passes = cfg->max_passes; d.f = cfg->screen_every; d.rule = cfg->rule;
+        d.certify = cfg->certify; d.cd_warps = cs.W;
+        set_plan(&Bt->shape, d);
         const char* env = getenv("GS_REFRESH_EXCESS");
         d.refresh_excess = env ? atoi(env) : 32;
         d.cd_gram = cs.mode;
@@ -1404,7 +1446,7 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
         o.passes = dpasses + b * T; o.gaps = dgaps + b * T; o.converged = dconv + b * T; o.n_active = dnact + b * T;
         o.T = (int)T;
         memset(&hsc[b], 0, sizeof(DevScalars));
-        hsc[b].eps = cfg->epsilon; hsc[b].y_norm_sq = Bt->ynsq[b];
+        hsc[b].eps = d.eps; hsc[b].y_norm_sq = Bt->ynsq[b];
     }
     CK(cudaMemcpyAsync(Bt->dprobs, probs.data(), B * sizeof(SolveDev), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(Bt->douts, outs.data(), B * sizeof(BatchOut), cudaMemcpyHostToDevice, st));
@@ -1416,7 +1458,7 @@ extern "C" int gs_batch_run_paths(gs_batch* Bt, const double* grids, int64_t T, 
     CK(cudaEventRecord(e0, st));
     COUNT_LAUNCH(1);
     const bool f64 = Bt->dtype == GS_DTYPE_F64;
-CK(f64 ? gs_launch_batch_f64(cs.R, st, Bt->dprobs, Bt->douts, (int)B, smem)
+    CK(f64 ? gs_launch_batch_f64(cs.R, st, Bt->dprobs, Bt->douts, (int)B, smem)
         : gs_launch_batch_f32(cs.R, st, Bt->dprobs, Bt->douts, (int)B, smem));
     CKL();
     CK(cudaEventRecord(e1, st));

@@ -184,7 +184,13 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             // speculative next window (same bound): its column slot was last read
             // before the previous window's barrier, its info slot two windows ago
             if (!last) {
-                if (w == 0) produce(s ^ 1, (k + 1) % kBInfo);
+                if (w == 0) {
+                    // rolling bound: the window two ahead of the last finished one is
+                    // selected under the current drift plus the allowance (never lowered,
+                    // so earlier gaps stay covered by their own window's bound)
+                    if (use_t) Dp = fmax(Dp, __dadd_ru(D, __dmul_ru(mfac, gstep)));
+                    produce(s ^ 1, (k + 1) % kBInfo);
+                }
                 uses[s ^ 1]++;
             }
             // ---- dots of the window: h_b and G(b,c), c < b
@@ -332,15 +338,18 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
                 ++n_req;
                 const int rpos = dsc->pos[ncommit - 1] + 1;
                 if (!last) {
-                    // the speculative window is stale: let its copies land first
-                    if (w == 0) blk_wait(bar_s + 8u * (s ^ 1), waited[s ^ 1], uses[s ^ 1] - 1, 12);
+                    // the speculative window is stale: every warp observes its phase
+                    // (mbarrier parity waits are only unambiguous one phase behind), and
+                    // only then may warp 0 issue the next phase into that slot
+                    blk_wait(bar_s + 8u * (s ^ 1), waited[s ^ 1], uses[s ^ 1] - 1, 12);
+                    if (NW > 1) named_bar(1, BT);
                 }
                 if (w == 0) {
                     cur = rpos;
                     if (cur < tb || cur > tend || (cur == tend && tend < m)) {
                         tb = cur; tend = cur;       // forces a reload at the next scan step
                     }
-                    Dp = __dadd_ru(D, __dmul_ru(mfac, gstep));
+                    Dp = fmax(Dp, __dadd_ru(D, __dmul_ru(mfac, gstep)));
                     produce(s ^ 1, (k + 1) % kBInfo);
                 }
                 uses[s ^ 1]++;
@@ -372,6 +381,7 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             ctl->epoch_nz = n_nz;
             ctl->n_requeue += n_req;
             ctl->n_cand += n_unc;
+            if (P.cd_prof) { ctl->n_win += (unsigned long long)(k + 1); ctl->n_mem += (unsigned long long)n_unc; }
             P.sc->visits += (unsigned long long)m;
             P.sc->uncertified += (unsigned long long)n_unc;
             P.sc->nonzero += (unsigned long long)n_nz;

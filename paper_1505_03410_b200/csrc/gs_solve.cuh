@@ -121,6 +121,9 @@ struct SolveDev {
     int csc_par;         // CSC CD: fully parallel waves (cd_epoch_csc_par)
     int* rowmark;        // [n] row map of cd_epoch_csc_par (kRowFree between waves)
     int blk_mfac;        // blocked-chain CD: window drift bound Dp = D + blk_mfac * gstep
+    int gemv_wide;       // dense GEMV: whole CTA per column (columns >= 16 KB), v in registers
+    int csc_short;       // CSC GEMV: 8 lanes per column (short columns), 32 columns per warp round
+    int smem_total;      // dynamic shared memory of the launch (bytes)
 };
 
 struct Group {
@@ -277,6 +280,189 @@ enum GMode : int { G_DUAL = 0, G_CERT = 1, G_MU = 2 };
 
 constexpr int kGStages = 4;     // TMA stages of the staged dense GEMV
 
+// ---------------------------------------------------------------------------
+// Wide-column dense GEMV (P.gemv_wide: columns of 16 KB and more, cfg2's
+// 40 KB f32 columns).  A whole column no longer fits several times in a
+// stage, so the warp-per-column form would leave 7 of 8 warps idle.  Here the
+// CTA streams its contiguous share of positions through a ring of whole-column
+// slots (cp.async.bulk, one mbarrier per slot) and ALL warps reduce each
+// column: thread t owns the 16-byte vectors t, t + 256, ... of every column
+// and keeps the matching entries of v in registers (no shared-memory reads of
+// v at all); per column one butterfly per warp and a fixed-order sum of the
+// warp partials by thread 0, which also runs the epilogue and re-issues the
+// slot.  One __syncthreads per column.
+// ---------------------------------------------------------------------------
+constexpr int kWideRows = 44;      // entries of v per thread: n <= 256 * 44 = 11264
+constexpr int kWideSlots = 8;
+
+template <typename T, class Epi>
+static __device__ __forceinline__ void group_gemv_wide(const Group& g, const SolveDev& P, const double* __restrict__ v,
+                                                    const int32_t* cols, int64_t m, int mode, unsigned char* stg,
+                                                    int64_t stg_bytes, Epi epilogue) {
+    constexpr int E = 16 / (int)sizeof(T);          // elements per 16-byte vector
+    constexpr int KV = kWideRows / E;               // vectors per thread
+    __shared__ unsigned long long s_wbar[kWideSlots];
+    __shared__ double s_wpart[2][8];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, W = blockDim.x >> 5;
+    const int n = P.n;
+    const T* X = (const T*)P.X;
+    const int64_t colb = P.ld * (int64_t)sizeof(T);
+    const int NS = (int)min((int64_t)kWideSlots, stg_bytes / colb);
+    const int nvec = (int)(P.ld / E);
+    const int64_t per = (m + g.G - 1) / g.G;
+    const int64_t lo = min(m, (int64_t)g.c * per), hi = min(m, lo + per);
+    const int nst = (int)(hi - lo);
+    const unsigned bar0 = smem_u32(&s_wbar[0]);
+    const unsigned stg0 = smem_u32(stg);
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&s_wbar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // this thread's entries of v (rows past n are zero: the column padding is zero too)
+    double th[KV * E];
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = (tid + k * 256) * E + e;
+            th[k * E + e] = r < n ? v[r] : 0.0;
+        }
+    }
+    __syncthreads();
+    auto issue = [&](int k) {                       // thread 0: column lo + k into slot k % NS
+        const int s = k % NS;
+        const int64_t i = lo + k;
+        const int64_t j = cols ? (int64_t)cols[i] : i;
+        const unsigned b = bar0 + 8u * s;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx_s(b, (unsigned)colb);
+        tma_bulk_g2s_s(stg0 + (unsigned)(s * colb), X + j * P.ld, (unsigned)colb, b);
+    };
+    if (tid == 0)
+        for (int k = 0; k < min(nst, NS); ++k) issue(k);
+    for (int k = 0; k < nst; ++k) {
+        const int s = k % NS;
+        const int64_t i = lo + k;
+        int64_t j = 0; double nrm = 0.0, bj = 0.0;
+        if (tid == 0) {
+            j = cols ? (int64_t)cols[i] : i;
+            nrm = __ldg(P.norms + j);
+            if (mode == G_CERT) bj = P.beta[j];
+        }
+        {
+            const unsigned b = bar0 + 8u * s, par = (unsigned)((k / NS) & 1);
+            if (!mbar_test_s(b, par)) {
+                const unsigned long long t0 = gtimer();
+                while (!mbar_test_s(b, par)) spin_guard(t0, 6, k, nst, (int)g.c, 0);
+            }
+        }
+        const uint4* base = reinterpret_cast<const uint4*>(stg + (size_t)s * colb);
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KV; ++kk) {
+            const int q = tid + kk * 256;
+            if (kk * 256 >= nvec) break;            // uniform
+            if (q < nvec) {
+                const uint4 raw = base[q];
+                if constexpr (E == 2) {
+                    a0 = fma(__hiloint2double((int)raw.y, (int)raw.x), th[kk * 2], a0);
+                    a1 = fma(__hiloint2double((int)raw.w, (int)raw.z), th[kk * 2 + 1], a1);
+                } else {
+                    a0 = fma((double)__uint_as_float(raw.x), th[kk * 4], a0);
+                    a1 = fma((double)__uint_as_float(raw.y), th[kk * 4 + 1], a1);
+                    a0 = fma((double)__uint_as_float(raw.z), th[kk * 4 + 2], a0);
+                    a1 = fma((double)__uint_as_float(raw.w), th[kk * 4 + 3], a1);
+                }
+            }
+        }
+        double sum = a0 + a1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) s_wpart[k & 1][w] = sum;
+        __syncthreads();                             // slot fully read, partials visible
+        if (tid == 0) {
+            double cval = 0.0;
+            for (int q = 0; q < W; ++q) cval += s_wpart[k & 1][q];
+            epilogue(i, j, cval, nrm, bj);
+            if (k + NS < nst) issue(k + NS);
+        }
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int s = 0; s < NS; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&s_wbar[s])) : "memory");
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Short-column CSC GEMV (P.csc_short: about 24 nonzeros per column or fewer,
+// cfg3's 20).  A warp takes 32 consecutive positions per round: lane l loads
+// the column pointers, norm (and beta) of position l; the columns are then
+// reduced by 8-lane groups, four columns at a time, with the loads of all
+// eight batches issued before the first gather (24 values + 24 row indices in
+// flight per lane).  Three shuffle steps per column instead of five, no idle
+// lanes, and the per-column epilogues run lane-parallel.
+// ---------------------------------------------------------------------------
+template <class Epi>
+static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, const SolveDev& P, const double* vv,
+                                                            const int32_t* cols, int64_t m, int mode, Epi epilogue) {
+    constexpr int T3 = 3;                            // unrolled trips of 8 nonzeros
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int sub = lane >> 3, sl = lane & 7;
+    const int64_t GW = (int64_t)g.G * W;
+    const int64_t nround = (m + 31) / 32;
+    for (int64_t rd = (int64_t)g.c * W + w; rd < nround; rd += GW) {
+        const int64_t i = rd * 32 + lane;
+        const bool valid = i < m;
+        const int64_t j = valid ? (cols ? (int64_t)cols[i] : i) : 0;
+        int64_t plo = 0, phi = 0;
+        double nrm = 0.0, bj = 0.0;
+        if (valid) {
+            plo = __ldg(P.indptr + j);
+            phi = __ldg(P.indptr + j + 1);
+            nrm = __ldg(P.norms + j);
+            if (mode == G_CERT) bj = P.beta[j];
+        }
+        double dv[8][T3];
+        int32_t iv[8][T3];
+        int64_t qlo[8], qhi[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int src = 4 * b + sub;
+            qlo[b] = __shfl_sync(FULL, plo, src) + sl;
+            qhi[b] = __shfl_sync(FULL, phi, src);
+#pragma unroll
+            for (int t = 0; t < T3; ++t) {
+                const int64_t q = qlo[b] + 8 * t;
+                const bool ok = q < qhi[b];
+                dv[b][t] = ok ? __ldg(P.data + q) : 0.0;
+                iv[b][t] = ok ? __ldg(P.indices + q) : 0;
+            }
+        }
+        double acc[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            double a = 0.0;
+#pragma unroll
+            for (int t = 0; t < T3; ++t) a = fma(dv[b][t], vv[iv[b][t]], a);
+            for (int64_t q = qlo[b] + 8 * T3; q < qhi[b]; q += 8) a = fma(__ldg(P.data + q), vv[__ldg(P.indices + q)], a);
+            acc[b] = a;
+        }
+        double cval = 0.0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            double a = acc[b];
+            a += __shfl_xor_sync(FULL, a, 4);
+            a += __shfl_xor_sync(FULL, a, 2);
+            a += __shfl_xor_sync(FULL, a, 1);
+            // column 4 b + sub sits in the lanes of group `sub`; lane l wants column l
+            const double got = __shfl_sync(FULL, a, (lane & 3) * 8);
+            if ((lane >> 2) == b) cval = got;
+        }
+        if (valid) epilogue(i, j, cval, nrm, bj);
+    }
+}
+
 template <typename T>
 static __device__ void group_gemv(const Group& g, const SolveDev& P, const double* v, const int32_t* cols, int64_t m,
                            int mode, double* out_c, float* out_t, double rho0, double gam, double radius,
@@ -284,7 +470,8 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
                            int* tile_valid = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = P.n;
-    const bool stage = n <= P.vs_cap;
+    const bool wide = !P.sparse && P.gemv_wide && stg != nullptr && (int64_t)P.smem_total >= 2 * P.ld * (int64_t)sizeof(T);
+    const bool stage = n <= P.vs_cap && !wide;
     if (stage) {
         for (int r = threadIdx.x; r < n + 2; r += blockDim.x) vs[r] = r < n ? v[r] : 0.0;
         __syncthreads();
@@ -309,7 +496,14 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             }
         }
     };
-    if (P.sparse) {
+    if (P.sparse && P.csc_short) {
+        group_gemv_csc_short(g, P, vv, cols, m, mode, epilogue);
+    } else if (wide) {
+        // vs is not staged in this mode: the ring takes the whole dynamic shared memory
+        group_gemv_wide<T>(g, P, v, cols, m, mode, stg, (int64_t)P.smem_total, epilogue);
+        if (tile_valid && threadIdx.x == 0) *tile_valid = 0;   // the CD threshold tile was overwritten
+        __syncthreads();
+    } else if (P.sparse) {
         for (int64_t i = (int64_t)g.c * W + w; i < m; i += GW) {
             const int64_t j = cols ? (int64_t)cols[i] : i;
             const double nrm = __ldg(P.norms + j);

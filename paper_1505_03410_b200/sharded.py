@@ -219,7 +219,8 @@ def _nonzero_norms(backend) -> np.ndarray:
     return np.asarray(norms) > 0
 
 
-def run_batch_sharded(X0, y0: np.ndarray, rows: np.ndarray, grids: np.ndarray, config: SolverConfig):
+def run_batch_sharded(X0, y0: np.ndarray, rows: np.ndarray, grids: np.ndarray, config: SolverConfig,
+                      epsilons: np.ndarray | None = None):
     """Independent problems sharded by problem index:
     rank g runs problems ``shard_range(B, g, world)`` with one CTA each on its
     own GPU (``BatchPathSolver``); X0 and y0 are replicated.  No collective on
@@ -236,7 +237,7 @@ def run_batch_sharded(X0, y0: np.ndarray, rows: np.ndarray, grids: np.ndarray, c
     out = None
     if hi > lo:
         bs = BatchPathSolver(X0, y0, rows[lo:hi])
-        out = bs.run_paths(grids[lo:hi], config)
+        out = bs.run_paths(grids[lo:hi], config, epsilons=None if epsilons is None else epsilons[lo:hi])
     dev = D._device()
     mx = max(D.shard_range(B, r, world)[1] - D.shard_range(B, r, world)[0] for r in range(world))
     pack = torch.zeros((mx, T, 4), dtype=torch.float64, device=dev)

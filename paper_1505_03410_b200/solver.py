@@ -285,8 +285,20 @@ class PathTimer:
         ms = ctypes.c_double()
         cnt = ctypes.c_int64()
         _lib.check(X._lib.gs_screen_timed(X.handle, _lib.f64p(c), float(radius), int(reps),
-                                          ctypes.byref(ms), ctypes.byref(cnt)))
+                                          ctypes.byref(ms), ctypes.byref(cnt), None))
         return ms.value
+
+    @staticmethod
+    def screen_pass_active(X, center: np.ndarray, radius: float) -> np.ndarray:
+        """Survivors of the fused in-kernel screening pass (the persistent
+        kernel's sequential screen, regions.py:129-139 semantics), ascending."""
+        c = np.ascontiguousarray(center, dtype=np.float64)
+        ms = ctypes.c_double()
+        cnt = ctypes.c_int64()
+        out = np.empty(X.n_cols, dtype=np.int32)
+        _lib.check(X._lib.gs_screen_timed(X.handle, _lib.f64p(c), float(radius), 1,
+                                          ctypes.byref(ms), ctypes.byref(cnt), _lib.i32p(out)))
+        return out[: cnt.value].astype(np.int64)
 
     @staticmethod
     def e2e_path_ms(case, grid, config, reps: int = 1):
@@ -345,10 +357,13 @@ class BatchPathSolver:
             self._lib.gs_batch_free(h)
             self._h = None
 
-    def run_paths(self, grids: np.ndarray, config: SolverConfig, want_betas: bool = False):
-        """grids: (B, T) non-increasing per row.  Returns a dict of (B, T)
-        arrays: passes, gaps, converged, n_active (+ betas (B, T, p)) and the
-        device time in ms."""
+    def run_paths(self, grids: np.ndarray, config: SolverConfig, want_betas: bool = False,
+                  epsilons: np.ndarray | None = None):
+        """grids: (B, T) non-increasing per row.  ``epsilons``: per-problem gap
+        tolerances (B,), overriding ``config.epsilon`` (the reference's solve
+        takes epsilon per problem, solver.py:37,226; configs[4] uses
+        1e-8 * ||y_b||^2).  Returns a dict of (B, T) arrays: passes, gaps,
+        converged, n_active (+ betas (B, T, p)) and the device time in ms."""
         if config.rule not in _BATCH_RULES:
             raise NotImplementedError(f"rule {config.rule.value!r} is not on the batched B200 path in this build")
         grids = np.ascontiguousarray(grids, dtype=np.float64)
@@ -357,6 +372,12 @@ class BatchPathSolver:
             raise ValueError("grids must have one row per problem")
         if np.any(np.diff(grids, axis=1) > 0):
             raise ValueError("grid must be non-increasing")
+        if epsilons is not None:
+            epsilons = np.ascontiguousarray(epsilons, dtype=np.float64)
+            if epsilons.shape != (B,):
+                raise ValueError("epsilons must have one entry per problem")
+            if not np.all(epsilons > 0):
+                raise ValueError("epsilon must be positive")
         cfg = _lib.SolveConfig(float(config.epsilon), int(config.max_passes), int(config.screen_every),
                                _GPU_RULES[config.rule], int(bool(config.certify)), _lib.CKPT_CB(), None)
         passes = np.empty((B, T), dtype=np.int64)
@@ -366,7 +387,7 @@ class BatchPathSolver:
         betas = np.empty((B, T, self.p)) if want_betas else None
         ms = ctypes.c_double()
         _lib.check(self._lib.gs_batch_run_paths(self._h, _lib.f64p(grids), T, ctypes.byref(cfg),
-                                                _lib.f64p(betas), _lib.i64p(passes), _lib.f64p(gaps),
+                                                _lib.f64p(epsilons), _lib.f64p(betas), _lib.i64p(passes), _lib.f64p(gaps),
                                                 _lib.i32p(conv), _lib.i64p(nact), ctypes.byref(ms)))
         out = dict(passes=passes, gaps=gaps, converged=conv.astype(bool), n_active=nact, device_ms=ms.value)
         if want_betas:

@@ -24,13 +24,14 @@ def test_batch_paths_match_oracle():
     bs = gs.BatchPathSolver(D0, y0, rows)
     grids = np.stack([gs.lambda_grid(bs.lambda_max[b], T, 2.0) for b in range(B)])
     eps = np.array([1e-8 * float(y0[rows[b]] @ y0[rows[b]]) for b in range(B)])
-    # one epsilon per run: use the smallest (all problems solved at least that tightly)
-    res = bs.run_paths(grids, gs.SolverConfig(epsilon=float(eps.min()), max_passes=100_000), want_betas=True)
+    # configs[4]: every problem stops at its own tolerance eps_b = 1e-8 ||y_b||^2
+    assert np.unique(eps).size == B
+    res = bs.run_paths(grids, gs.SolverConfig(epsilon=1.0, max_passes=100_000), want_betas=True, epsilons=eps)
     for b in range(B):
         Xb = np.asfortranarray(X0[rows[b]])
         yb = y0[rows[b]]
         ref = O.run_path(O.DesignMatrix(Xb), yb, grids[b],
-                         O.SolverConfig(epsilon=float(eps.min()), max_passes=100_000))
+                         O.SolverConfig(epsilon=float(eps[b]), max_passes=100_000))
         yy = float(yb @ yb)
         for t in range(T):
             st = ref.states[t]

@@ -228,3 +228,59 @@ def test_cd_pipeline_stress(n):
             gs.cd_pass(st, prob)
         assert np.array_equal(np.flatnonzero(st.beta), np.flatnonzero(b_ref))
         np.testing.assert_allclose(st.beta, b_ref, rtol=0, atol=1e-10 * max(1, np.abs(b_ref).max()))
+
+
+def _fused_screen_case(kind):
+    rng = np.random.default_rng(21)
+    if kind == "dense_f64_wide":          # 4096 x 8 B = 32 KB columns: whole-CTA column reduction
+        n, p = 4096, 900
+        Xh = np.asfortranarray(rng.standard_normal((n, p)) / np.sqrt(n))
+    elif kind == "dense_f32_wide":        # cfg2's column shape: 10000 x 4 B = 40 KB
+        n, p = 10_000, 700
+        Xh = np.asfortranarray((rng.standard_normal((n, p)) / np.sqrt(n)).astype(np.float32))
+    elif kind == "dense_f32_odd_wide":    # wide with a ragged last vector per thread
+        n, p = 5003, 450
+        Xh = np.asfortranarray((rng.standard_normal((n, p)) / np.sqrt(n)).astype(np.float32))
+    elif kind == "dense_f64_staged":      # cfg1's column shape (TMA-staged warp-per-column form)
+        n, p = 1000, 3000
+        Xh = np.asfortranarray(rng.standard_normal((n, p)) / np.sqrt(n))
+    elif kind == "csc_short":             # cfg3's column shape: 20 nonzeros per column
+        n, p = 20_000, 6000
+        idx = np.concatenate([np.sort(rng.choice(n, 20, replace=False)) for _ in range(p)])
+        Xh = sp.csc_matrix((rng.lognormal(size=20 * p) / np.sqrt(20.0), idx, np.arange(0, 20 * p + 1, 20)),
+                           shape=(n, p))
+    elif kind == "csc_short_ragged":      # 0 .. 40 nonzeros per column, some empty, some past the unrolled trips
+        n, p = 3000, 5000
+        lens = rng.integers(0, 41, p)
+        lens[::97] = 0
+        idx = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens] + [np.empty(0, np.int64)])
+        ptr = np.concatenate([[0], np.cumsum(lens)])
+        Xh = sp.csc_matrix((rng.lognormal(size=int(ptr[-1])) / 4.0, idx.astype(np.int32), ptr), shape=(n, p))
+    else:                                 # long CSC columns: warp-per-column form
+        n, p = 2000, 1200
+        Xh = sp.random(n, p, density=0.05, random_state=np.random.RandomState(3), format="csc")
+        Xh.sort_indices()
+    return Xh, rng
+
+
+@pytest.mark.parametrize("kind", ["dense_f64_wide", "dense_f32_wide", "dense_f32_odd_wide", "dense_f64_staged",
+                                  "csc_short", "csc_short_ragged", "csc_long"])
+def test_fused_screen_pass_matches_oracle(kind):
+    """The persistent kernel's fused full-p screening pass (group_gemv G_MU in
+    each of its GEMV forms) keeps exactly the oracle's survivors, except
+    features within 1e-10 of the 1 - 1e-9 threshold (regions.py:129-139)."""
+    Xh, rng = _fused_screen_case(kind)
+    X64 = Xh.astype(np.float64) if not sp.issparse(Xh) else Xh
+    D = gs.DesignMatrix(Xh)
+    Dor = O.DesignMatrix(np.asfortranarray(X64) if not sp.issparse(Xh) else X64)
+    n = Xh.shape[0]
+    y = rng.standard_normal(n)
+    lmax, _ = Dor.max_abs_correlation(y)
+    c = y / lmax
+    for r in (0.0, 0.02, 0.2):
+        b = O.screen(O.Sphere(center=c, radius=r), Dor)
+        a = gs.PathTimer.screen_pass_active(D, c, r)
+        near = np.abs(b.mu - (1 - gs.SCREEN_SAFETY)) <= 1e-10
+        diff = np.setxor1d(a, b.active_set)
+        assert np.all(near[diff]), (kind, r, diff[:5])
+        assert a.size > 0 or b.active_set.size == 0

@@ -18,8 +18,8 @@ D0 = gs.DesignMatrix(X0)
 bs = gs.BatchPathSolver(D0, y0, rows)
 t2 = time.perf_counter()
 grids = np.stack([gs.lambda_grid(bs.lambda_max[b], T, 2.0) for b in range(B)])
-eps = min(1e-8 * float(y0[rows[b]] @ y0[rows[b]]) for b in range(B))
-res = bs.run_paths(grids, gs.SolverConfig(epsilon=eps, max_passes=100_000))
+eps = np.array([1e-8 * float(y0[rows[b]] @ y0[rows[b]]) for b in range(B)])
+res = bs.run_paths(grids, gs.SolverConfig(epsilon=1.0, max_passes=100_000), epsilons=eps)
 t3 = time.perf_counter()
 print(json.dumps(dict(config="cfg4", B=B, p=p, T=T, gen_s=t1 - t0, setup_s=t2 - t1, run_s=t3 - t2,
                       device_ms=res["device_ms"], epochs_total=int(res["passes"].sum()),

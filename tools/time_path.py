@@ -11,6 +11,7 @@ ap.add_argument("name", nargs="?", default="cfg0")
 ap.add_argument("p", nargs="?", type=int, default=None)
 ap.add_argument("--once", action="store_true", help="time the first (cold) path only")
 ap.add_argument("--lambdas", type=int, default=None, help="first T lambdas only")
+ap.add_argument("--per-lambda", action="store_true", help="add per-lambda epochs / visits / uncertified / cd_ms")
 a = ap.parse_args()
 name = a.name
 kw = {} if a.p is None else {"p": a.p}
@@ -40,4 +41,9 @@ out = dict(config=name, upload_s=t1 - t0, path_s_first=t2 - t1, path_s=(t3 - t2)
            skipped=int(sum(x["cd_skipped"] for x in st)),
            requeues=int(sum(x["cd_requeues"] for x in st)),
            converged=int(res.converged.sum()))
+if a.per_lambda:
+    out["per_lambda"] = [dict(t=t, epochs=int(s.passes_done), m_end=int(s.active.size), visits=int(x["cd_visits"]),
+                              unc=int(x["cd_uncertified"]), nz=int(x["cd_nonzero"]), cd_ms=float(x["cd_ms"]),
+                              refresh=int(x["n_refresh"]), refresh_ms=float(x["refresh_ms"]), ckpt_ms=float(x["ckpt_ms"]))
+                         for t, (s, x) in enumerate(zip(res.states, st))]
 print(json.dumps(out))
