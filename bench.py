@@ -1,6 +1,6 @@
 """Benchmark: Lasso-path wall time to gap 1e-8 (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg0|cfg1|cfg2|cfg3|cfg4] [--impl ours|reference]
 
 A "step" is one full warm-started Gap Safe Lasso path over the config's
 lambda grid.  ``value`` is the path wall time measured on
@@ -101,9 +101,23 @@ def _dist():
     return ws, rank, local
 
 
-def _make_case(name):
+def _init_ranks(ws, local):
+    """One process per GPU (NCCL).  When the box has fewer GPUs than ranks (the
+    1-GPU test box), ranks share devices and the host collectives run over
+    gloo -- no kernel of one rank ever waits on another rank."""
+    import torch
+    import torch.distributed as dist
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl" if ndev >= ws else "gloo")
+    return dev
+
+
+def _make_case(name, p=None):
     from paper_1505_03410_b200 import synth
-    return synth.by_name(name)
+    return synth.by_name(name, **({} if p is None else {"p": int(p)}))
 
 
 def _grid(lmax, case):
@@ -177,7 +191,7 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    case = _make_case(args.config)
+    case = _make_case(args.config, args.p)
     from oracle import gapsafe_oracle as O
     O.build_kernels()
     Xo = O.DesignMatrix(case.X)
@@ -236,12 +250,9 @@ def run_ours(args):
     import paper_1505_03410_b200 as gs
     from paper_1505_03410_b200 import _lib
     if ws > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        local = _init_ranks(ws, local)
     _lib.init_device(local)
-    case = _make_case(args.config)
+    case = _make_case(args.config, args.p)
     n, p = case.X.shape
     X = gs.DesignMatrix(case.X)
     dev = gs.DeviceSolver(X, case.y)
@@ -353,6 +364,159 @@ def run_ours(args):
     return 0
 
 
+def run_cfg4(args):
+    """configs[4]: B bootstrap problems (n = 500 rows drawn with replacement from
+    the shared 1000 x p design), each a 50-lambda path to lambda_max / 100 at
+    its own tolerance eps_b = 1e-8 ||y_b||^2, sharded by problem index over
+    the ranks (sharded.run_batch_sharded: no collective on the data path).  A
+    step is the whole batch; the time is the max over ranks of the device time
+    of the rank's persistent batch kernel.  Total work is fixed: "strong"."""
+    ws, rank, local = _dist()
+    import paper_1505_03410_b200 as gs
+    from paper_1505_03410_b200 import _lib, sharded, synth
+    from paper_1505_03410_b200 import dist as D
+    if ws > 1:
+        local = _init_ranks(ws, local)
+    _lib.init_device(local)
+    B, T = int(args.problems), 50
+    X0, y0, _ = synth.cfg4_shared(p=args.p or 50_000)
+    rows = np.stack([synth.cfg4_rows(b) for b in range(B)]).astype(np.int32)
+    D0 = gs.DesignMatrix(X0)
+    lo, hi = D.shard_range(B, rank, ws)
+    t0 = time.perf_counter()
+    bs = gs.BatchPathSolver(D0, y0, rows[lo:hi]) if hi > lo else None
+    setup_s = time.perf_counter() - t0
+    lmax = bs.lambda_max if bs is not None else np.zeros(0)
+    grids = np.stack([gs.lambda_grid(lmax[b - lo], T, 2.0) for b in range(lo, hi)]) if hi > lo else np.zeros((0, T))
+    eps = np.array([1e-8 * float(y0[rows[b]] @ y0[rows[b]]) for b in range(lo, hi)])
+    cfg = gs.SolverConfig(epsilon=1.0, max_passes=100_000)
+
+    def step():
+        if bs is None:
+            return None, 0.0
+        out = bs.run_paths(grids, cfg, epsilons=eps)
+        return out, out["device_ms"]
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup if not args.quick else 0):
+        step()
+    barrier()
+    l0 = _lib.launch_count()
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            out, dms = step()
+            wall = (time.perf_counter() - t0) * 1e3
+            ms.append((dms, wall))
+    launches = (_lib.launch_count() - l0) / args.steps
+    barrier()
+    ms_step = statistics.mean(m[0] for m in ms)
+    e2e_ms = statistics.mean(m[1] for m in ms) + setup_s * 1e3      # + gather / norms / lambda_max of the shard
+    if ws > 1:
+        ms_step = D.max_over_ranks(ms_step)
+        e2e_ms = D.max_over_ranks(e2e_ms)
+    n, p = rows.shape[1], X0.shape[1]
+    peak, peak_kind = _peaks()
+    scr_bytes = X0.shape[0] * p * 8 + p * 9 + X0.shape[0] * 8
+    scr_ms = gs.PathTimer.screen_pass_ms(D0, y0 / float(np.max(np.abs(X0.T @ y0))), 1e-3, reps=20)
+    line = {"metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, SURVEY.md §8(d))",
+            "config": {"workload": "cfg4", "problems": B, "n": int(n), "p": int(p), "lambdas": T, "tol": 1e-8,
+                       "eps": "per problem, 1e-8 ||y_b||^2", "screen_every": 10, "rule": "gap_sphere",
+                       "l2": f"{hi - lo} resampled designs of {n * p * 8 / 1e6:.0f} MB each > 126 MB L2"},
+            "parallelism": f"problems sharded over {ws} rank(s)", "clocks": clk.summary(), "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "k_screen_full on the shared design", "achieved": scr_bytes / (scr_ms * 1e-3) / 1e9,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": scr_bytes / (scr_ms * 1e-3) / 1e9 / peak, "traffic": None,
+                         "bytes_per_launch": scr_bytes, "launch_ms": scr_ms},
+            "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": int(X0.nbytes + y0.nbytes + rows[lo:hi].nbytes),
+                    "d2h_bytes_per_step": int((hi - lo) * T * 28)}}
+    if out is not None:
+        line["path"] = {"epochs": int(out["passes"].sum()), "converged": int(out["converged"].sum()), "of": int((hi - lo) * T),
+                        "rank0_problems": [int(lo), int(hi)]}
+    ok = True
+    if rank == 0 and not args.no_cpu and out is not None:
+        # parity + CPU baseline: the oracle on problem `lo`, first lambdas within the budget
+        from oracle import gapsafe_oracle as O
+        Xb = np.asfortranarray(X0[rows[lo]])
+        yb = y0[rows[lo]]
+        ref = O.run_path(O.DesignMatrix(Xb), yb, grids[0], O.SolverConfig(epsilon=float(eps[0]), max_passes=100_000),
+                         cache_lambda_max=True, time_budget_s=args.cpu_budget)
+        k = len(ref.states)
+        same = all(int(out["passes"][0, t]) == ref.states[t].passes_done and
+                   int(out["n_active"][0, t]) == ref.states[t].active.size for t in range(k))
+        ok = bool(same)
+        line["parity"] = {"problem": int(lo), "lambdas_compared": k, "epochs_and_active_sizes_equal": ok, "ok": ok}
+        line["cpu_baseline"] = {"value": float(sum(ref.timings)), "unit": "s", "cores": len(os.sched_getaffinity(0)),
+                                "kind": "port", "sample": f"first {k} of {T} lambdas of problem {lo} (1 of {B} problems; oracle)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0 if ok else 3
+
+
+def run_cfg2_sharded(args):
+    """configs[2] at N > 1: the design is sharded by contiguous column blocks
+    (each rank generates and uploads only its own columns), the full-p
+    screening pass runs on every rank over 1/N of the design, and the
+    survivors' columns are gathered device to device to rank 0 for the solve
+    (sharded.run_path_sharded).  Total work is fixed: "strong"."""
+    ws, rank, local = _dist()
+    import paper_1505_03410_b200 as gs
+    from paper_1505_03410_b200 import _lib, sharded, synth
+    from paper_1505_03410_b200 import dist as D
+    local = _init_ranks(ws, local)
+    _lib.init_device(local)
+    p = int(args.p or 1_000_000)
+    lo, hi = D.shard_range(p, rank, ws)
+    Xs, y, _, meta = synth.cfg2_streamed(p=p, col_range=(lo, hi))
+    be = sharded.DeviceBackend(Xs, y)
+    v, j = be.max_abs_correlation(y)
+    lmax, _ = D.argmax_over_ranks(float(v), lo + int(j))
+    grid = gs.lambda_grid(lmax, 50, float(np.log10(20.0)))
+    cfg = gs.SolverConfig(epsilon=1e-5 * float(y @ y), max_passes=100_000)
+    import torch
+    import torch.distributed as dist
+
+    def one_path():
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = sharded.run_path_sharded(be, y, grid, cfg, p, lo)
+        torch.cuda.synchronize()
+        return res, (time.perf_counter() - t0) * 1e3
+
+    for _ in range(0 if args.quick else 1):
+        one_path()
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            res, t = one_path()
+            ms.append(t)
+    ms_step = D.max_over_ranks(statistics.mean(ms))
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
+                "warmup": 1, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64 arithmetic on f32 storage", "data": "synthetic (seeded generator, SURVEY.md §8(d))",
+                "config": {"workload": "cfg2", "n": int(y.size), "p": p, "lambdas": 50, "tol": 1e-5, "rule": "gap_sphere",
+                           "instance": meta},
+                "parallelism": f"columns sharded over {ws} ranks; X_A gathered to rank 0 (device to device)",
+                "clocks": clk.summary(),
+                "timing": "host clock between barriers + device synchronisation (the path is host-driven across ranks)",
+                "path": {"epochs": int(sum(s.passes_done for s in res.states)), "converged": int(res.converged.sum())}}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def _spawn_ranks(args) -> int:
     """``--gpus N`` outside torchrun: relaunch this script as N ranks on one
     node (one process per GPU), the way the driver does."""
@@ -376,6 +540,9 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=900.0,
                     help="reference arm: stop starting new full paths after this many seconds")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--p", type=int, default=None, help="column count override (cfg2 / cfg4 prefixes)")
+    ap.add_argument("--problems", type=int, default=256, help="cfg4: number of bootstrap problems")
+    ap.add_argument("--quick", action="store_true", help="cfg2 / cfg4: skip the warm-up steps (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -383,6 +550,10 @@ def main():
         return _spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "cfg4":
+        return run_cfg4(args)
+    if args.config == "cfg2" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_cfg2_sharded(args)
     return run_ours(args)
 
 

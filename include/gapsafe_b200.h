@@ -60,6 +60,23 @@ int64_t gs_launch_count(void);
  * norms_sq: optional host column norms^2 (else computed on the device). */
 int gs_matrix_dense(const void *X, int dtype, int64_t n, int64_t p, int64_t ld_host,
                     const double *norms_sq, gs_matrix **out);
+/* The same from a DEVICE buffer (column j at X_dev + j*ld_dev): device-to-device
+ * copy into owned storage.  The column-sharded path builds
+ * the survivors' sub-design X_A from columns received over NCCL without a
+ * host round trip.  The caller synchronises the producer of X_dev first. */
+int gs_matrix_dense_dev(const void *X_dev, int dtype, int64_t n, int64_t p, int64_t ld_dev, gs_matrix **out);
+/* A dense design built block by block (designs too large for one host array,
+ * e.g. configs[2] at 40 GB): allocate zeroed device storage, upload column
+ * blocks [j0, j0+k) from a host buffer (column-major, ld_host rows; reusable
+ * on return), then finalize (column norms).  No other call is valid on the
+ * matrix before gs_matrix_dense_finalize. */
+int gs_matrix_dense_alloc(int dtype, int64_t n, int64_t p, gs_matrix **out);
+int gs_matrix_dense_set_columns(gs_matrix *M, int64_t j0, int64_t k, const void *X, int64_t ld_host);
+int gs_matrix_dense_finalize(gs_matrix *M);
+/* Columns idx[0..k) of a dense design into a DEVICE buffer (ld_dst rows per
+ * column, rows past n zeroed): the send buffer of that gather.  Returns after
+ * the copy completed. */
+int gs_matrix_gather_columns_dev(const gs_matrix *M, const int64_t *idx, int64_t k, void *dst_dev, int64_t ld_dst);
 /* Canonical CSC (sorted, deduplicated), design_matrix.py:37-43. */
 int gs_matrix_csc(const double *data, const int32_t *indices, const int64_t *indptr,
                   int64_t n, int64_t p, const double *norms_sq, gs_matrix **out);

@@ -92,6 +92,11 @@ SIGNATURES = {
                                 ctypes.c_int, ctypes.POINTER(SolveResult)]),
     "gs_solver_free": (None, [c_vp]),
     "gs_solver_timer": (c_i32, [c_vp, ctypes.c_int, P_f64]),
+    "gs_matrix_dense_alloc": (c_i32, [c_i32, c_i64, c_i64, ctypes.POINTER(c_vp)]),
+    "gs_matrix_dense_set_columns": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64]),
+    "gs_matrix_dense_finalize": (c_i32, [c_vp]),
+    "gs_matrix_dense_dev": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, ctypes.POINTER(c_vp)]),
+    "gs_matrix_gather_columns_dev": (c_i32, [c_vp, P_i64, c_i64, c_vp, c_i64]),
     "gs_screen_timed": (c_i32, [c_vp, P_f64, c_dbl, ctypes.c_int, P_f64, P_i64, P_i32]),
     "gs_host_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
     "gs_host_free": (None, [c_vp]),

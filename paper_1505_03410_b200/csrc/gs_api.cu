@@ -224,6 +224,121 @@ extern "C" int gs_matrix_csc(const double* data, const int32_t* indices, const i
     return GS_OK;
 }
 
+// dense design from a DEVICE buffer (column-major, ld_dev rows per column):
+// device-to-device copy into owned storage, norms on the device.  Used by the
+// column-sharded path: the survivors' columns arrive over NCCL in device
+// memory and never touch the host (sharded.py).
+extern "C" int gs_matrix_dense_dev(const void* X_dev, int dtype, int64_t n, int64_t p, int64_t ld_dev,
+                                   gs_matrix** out) {
+    TRY(ensure_device());
+    if (n < 1 || p < 1) return fail(GS_ERR_VALUE, "matrix must have at least one row and column");
+    if (n > (1 << 30)) return fail(GS_ERR_VALUE, "too many rows");
+    if (dtype != GS_DTYPE_F64 && dtype != GS_DTYPE_F32) return fail(GS_ERR_VALUE, "dtype must be f64 or f32");
+    if (ld_dev < n) return fail(GS_ERR_VALUE, "ld_dev must be at least n");
+    gs_matrix* M = new gs_matrix();
+    M->dtype = dtype; M->n = n; M->p = p;
+    const size_t es = dtype == GS_DTYPE_F64 ? 8 : 4;
+    const int64_t align = dtype == GS_DTYPE_F64 ? 2 : 4;
+    M->ld = (n + align - 1) / align * align;
+    int rc;
+    if ((rc = [&]() -> int {
+            CK(cudaStreamCreateWithFlags(&M->st, cudaStreamNonBlocking));
+            CK(cudaMalloc(&M->X, (size_t)M->ld * p * es));
+            M->bytes += (int64_t)M->ld * p * es;
+            if (M->ld != n) CK(cudaMemsetAsync(M->X, 0, (size_t)M->ld * p * es, M->st));
+            // the source was produced on another stream (torch / NCCL): the caller
+            // synchronises it before this call; the copy itself is stream-ordered here
+            CK(cudaMemcpy2DAsync(M->X, M->ld * es, X_dev, ld_dev * es, n * es, p, cudaMemcpyDeviceToDevice, M->st));
+            return matrix_norms(M, nullptr);
+        }()) != GS_OK) {
+        matrix_release(M);
+        return rc;
+    }
+    *out = M;
+    return GS_OK;
+}
+
+// Dense design built block by block (designs larger than a comfortable host
+// array: configs[2] is 40 GB): allocate zeroed device storage, upload column
+// blocks from (reusable) host buffers, then compute the norms.
+extern "C" int gs_matrix_dense_alloc(int dtype, int64_t n, int64_t p, gs_matrix** out) {
+    TRY(ensure_device());
+    if (n < 1 || p < 1) return fail(GS_ERR_VALUE, "matrix must have at least one row and column");
+    if (n > (1 << 30)) return fail(GS_ERR_VALUE, "too many rows");
+    if (dtype != GS_DTYPE_F64 && dtype != GS_DTYPE_F32) return fail(GS_ERR_VALUE, "dtype must be f64 or f32");
+    gs_matrix* M = new gs_matrix();
+    M->dtype = dtype; M->n = n; M->p = p;
+    const size_t es = dtype == GS_DTYPE_F64 ? 8 : 4;
+    const int64_t align = dtype == GS_DTYPE_F64 ? 2 : 4;
+    M->ld = (n + align - 1) / align * align;
+    int rc;
+    if ((rc = [&]() -> int {
+            CK(cudaStreamCreateWithFlags(&M->st, cudaStreamNonBlocking));
+            CK(cudaMalloc(&M->X, (size_t)M->ld * p * es));
+            M->bytes += (int64_t)M->ld * p * es;
+            CK(cudaMemsetAsync(M->X, 0, (size_t)M->ld * p * es, M->st));
+            CK(cudaStreamSynchronize(M->st));
+            return GS_OK;
+        }()) != GS_OK) {
+        matrix_release(M);
+        return rc;
+    }
+    *out = M;
+    return GS_OK;
+}
+
+extern "C" int gs_matrix_dense_set_columns(gs_matrix* M, int64_t j0, int64_t k, const void* X, int64_t ld_host) {
+    if (M->sparse || M->norms) return fail(GS_ERR_VALUE, "set_columns needs a dense design that is not finalized yet");
+    if (j0 < 0 || k < 0 || j0 + k > M->p) return fail(GS_ERR_INDEX, "column block out of range");
+    if (ld_host < M->n) return fail(GS_ERR_VALUE, "ld_host must be at least n");
+    if (k == 0) return GS_OK;
+    const size_t es = M->dtype == GS_DTYPE_F64 ? 8 : 4;
+    CK(cudaMemcpy2DAsync((char*)M->X + (size_t)j0 * M->ld * es, M->ld * es, X, ld_host * es, M->n * es, k,
+                         cudaMemcpyHostToDevice, M->st));
+    CK(cudaStreamSynchronize(M->st));      // the host buffer may be reused on return
+    return GS_OK;
+}
+
+extern "C" int gs_matrix_dense_finalize(gs_matrix* M) {
+    if (M->sparse || M->norms) return fail(GS_ERR_VALUE, "finalize needs a dense design that is not finalized yet");
+    return matrix_norms(M, nullptr);
+}
+
+template <typename T>
+static __global__ void k_gather_cols(const T* __restrict__ X, int64_t ld, int n, const int64_t* __restrict__ idx,
+                                     int64_t k, T* __restrict__ dst, int64_t ld_dst) {
+    // one block per gathered column (grid-stride), threads over rows; rows n..ld_dst-1 zeroed
+    for (int64_t c = blockIdx.x; c < k; c += gridDim.x) {
+        const T* src = X + idx[c] * ld;
+        T* d = dst + c * ld_dst;
+        for (int64_t r = threadIdx.x; r < ld_dst; r += blockDim.x) d[r] = r < n ? src[r] : (T)0;
+    }
+}
+
+// columns idx[0..k) of a dense design into a DEVICE buffer (column-major,
+// ld_dst rows per column): the send buffer of the X_A gather
+extern "C" int gs_matrix_gather_columns_dev(const gs_matrix* M, const int64_t* idx, int64_t k, void* dst_dev,
+                                            int64_t ld_dst) {
+    TRY(ensure_device());
+    if (M->sparse) return fail(GS_ERR_VALUE, "column gather needs a dense design");
+    if (ld_dst < M->n) return fail(GS_ERR_VALUE, "ld_dst must be at least n");
+    if (k == 0) return GS_OK;
+    for (int64_t c = 0; c < k; ++c)
+        if (idx[c] < 0 || idx[c] >= M->p) return fail(GS_ERR_INDEX, "column index out of range");
+    int64_t* didx = nullptr;
+    TRY(dalloc(&didx, k));
+    struct Free { void* q; ~Free() { cudaFree(q); } } guard{didx};
+    CK(cudaMemcpyAsync(didx, idx, k * 8, cudaMemcpyHostToDevice, M->st));
+    const unsigned grid = (unsigned)std::min<int64_t>(k, 148 * 8);
+    if (M->dtype == GS_DTYPE_F64)
+        k_gather_cols<double><<<grid, 256, 0, M->st>>>((const double*)M->X, M->ld, (int)M->n, didx, k, (double*)dst_dev, ld_dst);
+    else
+        k_gather_cols<float><<<grid, 256, 0, M->st>>>((const float*)M->X, M->ld, (int)M->n, didx, k, (float*)dst_dev, ld_dst);
+    CKL();
+    CK(cudaStreamSynchronize(M->st));     // the buffer is handed to another stream (NCCL) next
+    return GS_OK;
+}
+
 extern "C" int gs_matrix_norms_sq(const gs_matrix* M, double* out) {
     CK(cudaMemcpyAsync(out, M->norms_sq, M->p * 8, cudaMemcpyDeviceToHost, M->st));
     CK(cudaStreamSynchronize(M->st));
@@ -506,20 +621,21 @@ static CdShape cd_shape(int64_t n) {
 static int cd_gram_default(int64_t n) { return (cd_shape(n).R <= 4 && cd_shape(n).W == 1) ? 1 : 0; }
 
 // blocked-chain consumer (gs_cd_blk.cuh): rows per thread R and compute warps
-// NW (no producer warp; warp 0 scans and issues the next window itself)
+// NW <= 7 (the warp after them is the producer: threshold scan + TMA issue)
 static CdShape cd_shape_blk(int64_t n) {
     if (n <= 32) return {1, 1};
     if (n <= 64) return {2, 1};
     if (n <= 128) return {4, 1};
     if (n <= 256) return {4, 2};
     if (n <= 512) return {4, 4};
-    if (n <= 1024) return {4, 8};
+    if (n <= 896) return {4, 7};
+    if (n <= 1120) return {5, 7};     // cfg1 (n = 1000): 5 rows per thread, 7 compute warps
     return {0, 0};
 }
 
 // dense CD plan: consumer mode (0 direct, 1 Gram windows, 2 blocked chain;
 // GS_CD_GRAM overrides), template R and warps.  The blocked chain is the
-// default wherever it applies (n <= 1024).
+// default wherever it applies (n <= 1120).
 struct CdPlan { int mode, R, W; };
 static CdPlan cd_plan(int64_t n) {
     const char* eg = getenv("GS_CD_GRAM");
@@ -581,8 +697,8 @@ static size_t solve_smem(const gs_matrix* M) {
     if (gemv_wide_for(M)) {
         // the column ring of the wide GEMV takes all of it: as many whole columns as fit (up to 8)
         const size_t colb = (size_t)M->ld * (M->dtype == GS_DTYPE_F64 ? 8 : 4);
-        const size_t cap = 224 * 1024;
-        const size_t want = std::min<size_t>(cap / colb, kWideSlots) * colb;
+        const size_t cap = 216 * 1024;          // leaves room for the kernels' static shared memory
+        const size_t want = std::min<size_t>((cap - kWidePartBytes) / colb, kWideSlots) * colb + kWidePartBytes;
         b = std::max(b, want);
     }
     return b;
@@ -595,6 +711,8 @@ static void set_plan(const gs_matrix* M, SolveDev& d) {
     d.gemv_wide = gemv_wide_for(M) ? 1 : 0;
     d.csc_short = csc_short_for(M) ? 1 : 0;
     d.smem_total = (int)solve_smem(M);
+    const char* ech = getenv("GS_CD_CHUNK");
+    d.cd_chunk_pos = M->sparse ? (ech ? atoi(ech) : 2048) : 0;
 }
 
 static int check_shape(const gs_matrix* M) {

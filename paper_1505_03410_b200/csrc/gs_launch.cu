@@ -9,6 +9,7 @@
             case 1: return gs_launch_solve_##SUF##_r1(st, dprobs, G, nprob, smem);                            \
             case 2: return gs_launch_solve_##SUF##_r2(st, dprobs, G, nprob, smem);                            \
             case 4: return gs_launch_solve_##SUF##_r4(st, dprobs, G, nprob, smem);                            \
+            case 5: return gs_launch_solve_##SUF##_r5(st, dprobs, G, nprob, smem);                            \
             case 8: return gs_launch_solve_##SUF##_r8(st, dprobs, G, nprob, smem);                            \
             default: return gs_launch_solve_##SUF##_r48(st, dprobs, G, nprob, smem);                          \
         }                                                                                                     \
@@ -18,6 +19,7 @@
             case 1: return gs_launch_cdpass_##SUF##_r1(st, dprobs, smem);                                     \
             case 2: return gs_launch_cdpass_##SUF##_r2(st, dprobs, smem);                                     \
             case 4: return gs_launch_cdpass_##SUF##_r4(st, dprobs, smem);                                     \
+            case 5: return gs_launch_cdpass_##SUF##_r5(st, dprobs, smem);                                     \
             case 8: return gs_launch_cdpass_##SUF##_r8(st, dprobs, smem);                                     \
             default: return gs_launch_cdpass_##SUF##_r48(st, dprobs, smem);                                   \
         }                                                                                                     \
@@ -28,6 +30,7 @@
             case 1: return gs_launch_batch_##SUF##_r1(st, dprobs, douts, B, smem);                            \
             case 2: return gs_launch_batch_##SUF##_r2(st, dprobs, douts, B, smem);                            \
             case 4: return gs_launch_batch_##SUF##_r4(st, dprobs, douts, B, smem);                            \
+            case 5: return gs_launch_batch_##SUF##_r5(st, dprobs, douts, B, smem);                            \
             case 8: return gs_launch_batch_##SUF##_r8(st, dprobs, douts, B, smem);                            \
             default: return cudaErrorInvalidValue;     /* batched problems: n <= 1792 */                       \
         }                                                                                                     \

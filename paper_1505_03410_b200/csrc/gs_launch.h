@@ -18,7 +18,7 @@ struct BatchOut;
     cudaError_t gs_launch_batch_##SUF##_r##R(cudaStream_t st, gs::SolveDev* dprobs, const gs::BatchOut* douts,       \
                                              int B, size_t smem);
 #define GS_DECLARE_LAUNCHERS(SUF)                                                                              \
-    GS_DECLARE_R(SUF, 1) GS_DECLARE_R(SUF, 2) GS_DECLARE_R(SUF, 4) GS_DECLARE_R(SUF, 8) GS_DECLARE_R(SUF, 48)    \
+    GS_DECLARE_R(SUF, 1) GS_DECLARE_R(SUF, 2) GS_DECLARE_R(SUF, 4) GS_DECLARE_R(SUF, 5) GS_DECLARE_R(SUF, 8) GS_DECLARE_R(SUF, 48)    \
     cudaError_t gs_launch_solve_##SUF(int R, cudaStream_t st, const gs::SolveDev* dprobs, int G, int nprob,        \
                                       size_t smem);                                                            \
     cudaError_t gs_launch_cdpass_##SUF(int R, cudaStream_t st, const gs::SolveDev* dprobs, size_t smem);           \

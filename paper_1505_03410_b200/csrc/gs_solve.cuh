@@ -48,6 +48,8 @@ struct SolveCtl {
     int64_t n_screen;
     // Gram-window consumer phase cycles (warp 0, clock64), GS_CD_PROF=1
     unsigned long long c_form, c_wait, c_red, c_chain, c_upd, n_win, n_mem;
+    unsigned long long c_w1[6];   // blocked chain: phase cycles of a second compute warp ([5]: producer idle)
+    unsigned long long c_pr[2];   // blocked chain: producer scan / descriptor + TMA issue cycles
 };
 
 static __device__ __forceinline__ unsigned long long gtimer() {
@@ -124,6 +126,7 @@ struct SolveDev {
     int gemv_wide;       // dense GEMV: whole CTA per column (columns >= 16 KB), v in registers
     int csc_short;       // CSC GEMV: 8 lanes per column (short columns), 32 columns per warp round
     int smem_total;      // dynamic shared memory of the launch (bytes)
+    int cd_chunk_pos;    // sparse CD: positions per re-anchored chunk of an epoch (0: whole epoch)
 };
 
 struct Group {
@@ -196,6 +199,26 @@ static __device__ __forceinline__ bool mbar_test_s(unsigned b, unsigned parity) 
 static __device__ __forceinline__ void tma_bulk_g2s_s(unsigned dst, const void* src, unsigned bytes, unsigned b) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+// The same with an L2 eviction-priority hint.  The group GEMVs stream the
+// whole active design (70-120 MB on cfg1) through L2 at every checkpoint and
+// refresh; without a hint they evict the few thousand columns the CD chain
+// re-reads every epoch, and the chain's TMA fetches then pay DRAM latency.
+// GEMV traffic is marked evict_first, the CD columns evict_last.
+static __device__ __forceinline__ unsigned long long l2_policy_evict_first() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+static __device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+static __device__ __forceinline__ void tma_bulk_g2s_hint(unsigned dst, const void* src, unsigned bytes, unsigned b,
+                                                         unsigned long long pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(b), "l"(pol) : "memory");
 }
 static __device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
 // CTA-scope acquire load / release store on shared memory (the load is a
@@ -280,6 +303,80 @@ enum GMode : int { G_DUAL = 0, G_CERT = 1, G_MU = 2 };
 
 constexpr int kGStages = 4;     // TMA stages of the staged dense GEMV
 
+// explicit shared-space loads on 32-bit addresses: a pointer that reaches a
+// helper through function arguments is generic to the compiler, and generic
+// loads of shared memory take the long-scoreboard path (LD.E, resolved at run
+// time) instead of LDS
+static __device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+static __device__ __forceinline__ double2 lds_f64x2(unsigned a) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+static __device__ __forceinline__ float4 lds_f32x4(unsigned a) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+static __device__ __forceinline__ float lds_f32x1(unsigned a) {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+static __device__ __forceinline__ uint4 lds_u32x4(unsigned a) {
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+// one column out of shared memory against a centre vector in shared memory,
+// both by 32-bit shared addresses; per-lane partition, accumulation order and
+// butterfly identical to ColDotS / ColDot2 (bit-identical results)
+template <typename T> struct ColDotSS;
+template <> struct ColDotSS<double> {
+    static __device__ __forceinline__ double run(unsigned x_s, unsigned v_s, int n, int lane) {
+        const int n2 = n >> 1;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n2; q += kWarp) {
+            const double2 xa = lds_f64x2(x_s + 16u * (unsigned)q);
+            const double2 vv = lds_f64x2(v_s + 16u * (unsigned)q);
+            a0 = fma(xa.x, vv.x, a0);
+            a1 = fma(xa.y, vv.y, a1);
+        }
+        if ((n & 1) && lane == 0) a0 = fma(lds_f64(x_s + 8u * (unsigned)(n - 1)), lds_f64(v_s + 8u * (unsigned)(n - 1)), a0);
+        double s = a0 + a1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        return s;
+    }
+};
+template <> struct ColDotSS<float> {
+    static __device__ __forceinline__ double run(unsigned x_s, unsigned v_s, int n, int lane) {
+        const int n4 = n >> 2;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < n4; q += kWarp) {
+            const float4 xa = lds_f32x4(x_s + 16u * (unsigned)q);
+            const double2 va = lds_f64x2(v_s + 32u * (unsigned)q), vb = lds_f64x2(v_s + 32u * (unsigned)q + 16u);
+            a0 = fma((double)xa.x, va.x, a0);
+            a1 = fma((double)xa.y, va.y, a1);
+            a0 = fma((double)xa.z, vb.x, a0);
+            a1 = fma((double)xa.w, vb.y, a1);
+        }
+        for (int r = (n4 << 2) + lane; r < n; r += kWarp)
+            a0 = fma((double)lds_f32x1(x_s + 4u * (unsigned)r), lds_f64(v_s + 8u * (unsigned)r), a0);
+        double s = a0 + a1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        return s;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // Wide-column dense GEMV (P.gemv_wide: columns of 16 KB and more, cfg2's
 // 40 KB f32 columns).  A whole column no longer fits several times in a
@@ -294,20 +391,25 @@ constexpr int kGStages = 4;     // TMA stages of the staged dense GEMV
 // ---------------------------------------------------------------------------
 constexpr int kWideRows = 44;      // entries of v per thread: n <= 256 * 44 = 11264
 constexpr int kWideSlots = 8;
+constexpr int kWidePartBytes = 2 * 32 * 8 * 8;     // warp partials of two epilogue batches (tail of the dynamic region)
 
 template <typename T, class Epi>
 static __device__ __forceinline__ void group_gemv_wide(const Group& g, const SolveDev& P, const double* __restrict__ v,
-                                                    const int32_t* cols, int64_t m, int mode, unsigned char* stg,
-                                                    int64_t stg_bytes, Epi epilogue) {
+                                                       const int32_t* cols, int64_t m, int mode, unsigned char* stg,
+                                                       int64_t stg_bytes, Epi epilogue) {
     constexpr int E = 16 / (int)sizeof(T);          // elements per 16-byte vector
     constexpr int KV = kWideRows / E;               // vectors per thread
+    constexpr int GV = 8;                           // vectors loaded per group (all issued before the first FMA)
+    constexpr int kEB = 32;                         // columns per epilogue batch (one lane each)
+    static_assert(kWidePartBytes == 2 * kEB * 8 * 8, "partials region");
     __shared__ unsigned long long s_wbar[kWideSlots];
-    __shared__ double s_wpart[2][8];
+    // warp partials of two epilogue batches: the last kWidePartBytes of the dynamic region
+    double (*s_wpart)[kEB][8] = reinterpret_cast<double (*)[kEB][8]>(stg + stg_bytes - kWidePartBytes);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, W = blockDim.x >> 5;
     const int n = P.n;
     const T* X = (const T*)P.X;
     const int64_t colb = P.ld * (int64_t)sizeof(T);
-    const int NS = (int)min((int64_t)kWideSlots, stg_bytes / colb);
+    const int NS = (int)min((int64_t)kWideSlots, (stg_bytes - kWidePartBytes) / colb);
     const int nvec = (int)(P.ld / E);
     const int64_t per = (m + g.G - 1) / g.G;
     const int64_t lo = min(m, (int64_t)g.c * per), hi = min(m, lo + per);
@@ -329,6 +431,7 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
         }
     }
     __syncthreads();
+    const unsigned long long pol_stream = l2_policy_evict_first();
     auto issue = [&](int k) {                       // thread 0: column lo + k into slot k % NS
         const int s = k % NS;
         const int64_t i = lo + k;
@@ -336,19 +439,28 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
         const unsigned b = bar0 + 8u * s;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx_s(b, (unsigned)colb);
-        tma_bulk_g2s_s(stg0 + (unsigned)(s * colb), X + j * P.ld, (unsigned)colb, b);
+        tma_bulk_g2s_hint(stg0 + (unsigned)(s * colb), X + j * P.ld, (unsigned)colb, b, pol_stream);
+    };
+    // epilogues run lane-parallel, one batch of kEB columns at a time, by the warp
+    // whose turn it is (batch index mod W): coalesced norm loads and mark stores,
+    // and no per-column serial tail on one thread
+    auto run_epilogues = [&](int kb0, int cnt) {    // columns kb0 .. kb0 + cnt of this CTA's share
+        if (lane < cnt) {
+            const int k = kb0 + lane;
+            const int64_t i = lo + k;
+            const int64_t j = cols ? (int64_t)cols[i] : i;
+            const double nrm = __ldg(P.norms + j);
+            const double bj = (mode == G_CERT) ? P.beta[j] : 0.0;
+            const double* pp = &s_wpart[(k / kEB) & 1][k % kEB][0];
+            double cval = 0.0;
+            for (int q = 0; q < W; ++q) cval += pp[q];
+            epilogue(i, j, cval, nrm, bj);
+        }
     };
     if (tid == 0)
         for (int k = 0; k < min(nst, NS); ++k) issue(k);
     for (int k = 0; k < nst; ++k) {
         const int s = k % NS;
-        const int64_t i = lo + k;
-        int64_t j = 0; double nrm = 0.0, bj = 0.0;
-        if (tid == 0) {
-            j = cols ? (int64_t)cols[i] : i;
-            nrm = __ldg(P.norms + j);
-            if (mode == G_CERT) bj = P.beta[j];
-        }
         {
             const unsigned b = bar0 + 8u * s, par = (unsigned)((k / NS) & 1);
             if (!mbar_test_s(b, par)) {
@@ -356,37 +468,48 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
                 while (!mbar_test_s(b, par)) spin_guard(t0, 6, k, nst, (int)g.c, 0);
             }
         }
-        const uint4* base = reinterpret_cast<const uint4*>(stg + (size_t)s * colb);
-        double a0 = 0.0, a1 = 0.0;
+        const unsigned base_s = stg0 + (unsigned)(s * colb);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-        for (int kk = 0; kk < KV; ++kk) {
-            const int q = tid + kk * 256;
-            if (kk * 256 >= nvec) break;            // uniform
-            if (q < nvec) {
-                const uint4 raw = base[q];
-                if constexpr (E == 2) {
-                    a0 = fma(__hiloint2double((int)raw.y, (int)raw.x), th[kk * 2], a0);
-                    a1 = fma(__hiloint2double((int)raw.w, (int)raw.z), th[kk * 2 + 1], a1);
-                } else {
-                    a0 = fma((double)__uint_as_float(raw.x), th[kk * 4], a0);
-                    a1 = fma((double)__uint_as_float(raw.y), th[kk * 4 + 1], a1);
-                    a0 = fma((double)__uint_as_float(raw.z), th[kk * 4 + 2], a0);
-                    a1 = fma((double)__uint_as_float(raw.w), th[kk * 4 + 3], a1);
+        for (int g0 = 0; g0 < KV; g0 += GV) {
+            if (g0 * 256 >= nvec) break;            // uniform
+            uint4 raw[GV];
+#pragma unroll
+            for (int u = 0; u < GV; ++u) {
+                const int q = tid + (g0 + u) * 256;
+                raw[u] = (g0 + u < KV && q < nvec) ? lds_u32x4(base_s + 16u * (unsigned)q) : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < GV; ++u) {
+                if (g0 + u < KV) {
+                    const int kk = g0 + u;
+                    if constexpr (E == 2) {
+                        if (u & 1) {
+                            a2 = fma(__hiloint2double((int)raw[u].y, (int)raw[u].x), th[kk * 2], a2);
+                            a3 = fma(__hiloint2double((int)raw[u].w, (int)raw[u].z), th[kk * 2 + 1], a3);
+                        } else {
+                            a0 = fma(__hiloint2double((int)raw[u].y, (int)raw[u].x), th[kk * 2], a0);
+                            a1 = fma(__hiloint2double((int)raw[u].w, (int)raw[u].z), th[kk * 2 + 1], a1);
+                        }
+                    } else {
+                        a0 = fma((double)__uint_as_float(raw[u].x), th[kk * 4], a0);
+                        a1 = fma((double)__uint_as_float(raw[u].y), th[kk * 4 + 1], a1);
+                        a2 = fma((double)__uint_as_float(raw[u].z), th[kk * 4 + 2], a2);
+                        a3 = fma((double)__uint_as_float(raw[u].w), th[kk * 4 + 3], a3);
+                    }
                 }
             }
         }
-        double sum = a0 + a1;
+        double sum = (a0 + a1) + (a2 + a3);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (lane == 0) s_wpart[k & 1][w] = sum;
+        if (lane == 0) s_wpart[(k / kEB) & 1][k % kEB][w] = sum;
         __syncthreads();                             // slot fully read, partials visible
-        if (tid == 0) {
-            double cval = 0.0;
-            for (int q = 0; q < W; ++q) cval += s_wpart[k & 1][q];
-            epilogue(i, j, cval, nrm, bj);
-            if (k + NS < nst) issue(k + NS);
-        }
+        if (tid == 0 && k + NS < nst) issue(k + NS);
+        if ((k % kEB) == kEB - 1 && w == ((k / kEB) % W)) run_epilogues(k - (kEB - 1), kEB);
     }
+    // the last, partial batch (its partials were published by the loop's last barrier)
+    if (nst % kEB != 0 && w == ((nst / kEB) % W)) run_epilogues(nst - nst % kEB, nst % kEB);
     __syncthreads();
     if (tid == 0)
         for (int s = 0; s < NS; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&s_wbar[s])) : "memory");
@@ -402,56 +525,74 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
 // flight per lane).  Three shuffle steps per column instead of five, no idle
 // lanes, and the per-column epilogues run lane-parallel.
 // ---------------------------------------------------------------------------
+// streamed once: read-only loads that do not allocate in L1 (with ~210 KB of the
+// SM's 256 KB in use as shared memory, the few L1 lines left would be evicted
+// between the trips that touch them and re-fetched from L2)
+static __device__ __forceinline__ double ldg_stream_f64(const double* p) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+static __device__ __forceinline__ int32_t ldg_stream_s32(const int32_t* p) {
+    int32_t v;
+    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 template <class Epi>
 static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, const SolveDev& P, const double* vv,
-                                                            const int32_t* cols, int64_t m, int mode, Epi epilogue) {
+                                                            const bool staged, const int32_t* cols, int64_t m, int mode,
+                                                            Epi epilogue) {
+    const unsigned vs_s = staged ? smem_u32(vv) : 0u;
+    auto vget = [&](int32_t r) -> double { return staged ? lds_f64(vs_s + 8u * (unsigned)r) : __ldg(vv + r); };
     constexpr int T3 = 3;                            // unrolled trips of 8 nonzeros
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int sub = lane >> 3, sl = lane & 7;
     const int64_t GW = (int64_t)g.G * W;
     const int64_t nround = (m + 31) / 32;
-    for (int64_t rd = (int64_t)g.c * W + w; rd < nround; rd += GW) {
+    // software pipeline over this warp's rounds: the column pointers of round
+    // r + 2 and the values / row indices of round r + 1 are in flight while
+    // round r is reduced (two register buffers, the loop unrolled by two)
+    struct Meta { int64_t j, plo, phi; double nrm, bj; bool valid; };
+    auto load_meta = [&](int64_t rd) {
+        Meta mt;
         const int64_t i = rd * 32 + lane;
-        const bool valid = i < m;
-        const int64_t j = valid ? (cols ? (int64_t)cols[i] : i) : 0;
-        int64_t plo = 0, phi = 0;
-        double nrm = 0.0, bj = 0.0;
-        if (valid) {
-            plo = __ldg(P.indptr + j);
-            phi = __ldg(P.indptr + j + 1);
-            nrm = __ldg(P.norms + j);
-            if (mode == G_CERT) bj = P.beta[j];
+        mt.valid = rd < nround && i < m;
+        mt.j = mt.valid ? (cols ? (int64_t)cols[i] : i) : 0;
+        mt.plo = 0; mt.phi = 0; mt.nrm = 0.0; mt.bj = 0.0;
+        if (mt.valid) {
+            mt.plo = __ldg(P.indptr + mt.j);
+            mt.phi = __ldg(P.indptr + mt.j + 1);
+            mt.nrm = __ldg(P.norms + mt.j);
+            if (mode == G_CERT) mt.bj = P.beta[mt.j];
         }
-        double dv[8][T3];
-        int32_t iv[8][T3];
-        int64_t qlo[8], qhi[8];
+        return mt;
+    };
+    struct Buf { double dv[8][T3]; int32_t iv[8][T3]; int64_t qlo[8], qhi[8]; };
+    auto load_buf = [&](const Meta& mt, Buf& B) {
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             const int src = 4 * b + sub;
-            qlo[b] = __shfl_sync(FULL, plo, src) + sl;
-            qhi[b] = __shfl_sync(FULL, phi, src);
+            B.qlo[b] = __shfl_sync(FULL, mt.plo, src) + sl;
+            B.qhi[b] = __shfl_sync(FULL, mt.phi, src);
 #pragma unroll
             for (int t = 0; t < T3; ++t) {
-                const int64_t q = qlo[b] + 8 * t;
-                const bool ok = q < qhi[b];
-                dv[b][t] = ok ? __ldg(P.data + q) : 0.0;
-                iv[b][t] = ok ? __ldg(P.indices + q) : 0;
+                const int64_t q = B.qlo[b] + 8 * t;
+                const bool ok = q < B.qhi[b];
+                B.dv[b][t] = ok ? ldg_stream_f64(P.data + q) : 0.0;
+                B.iv[b][t] = ok ? ldg_stream_s32(P.indices + q) : 0;
             }
         }
-        double acc[8];
+    };
+    auto reduce_buf = [&](int64_t rd, const Meta& mt, const Buf& B) {
+        double cval = 0.0;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             double a = 0.0;
 #pragma unroll
-            for (int t = 0; t < T3; ++t) a = fma(dv[b][t], vv[iv[b][t]], a);
-            for (int64_t q = qlo[b] + 8 * T3; q < qhi[b]; q += 8) a = fma(__ldg(P.data + q), vv[__ldg(P.indices + q)], a);
-            acc[b] = a;
-        }
-        double cval = 0.0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            double a = acc[b];
+            for (int t = 0; t < T3; ++t) a = fma(B.dv[b][t], vget(B.iv[b][t]), a);
+            for (int64_t q = B.qlo[b] + 8 * T3; q < B.qhi[b]; q += 8) a = fma(__ldg(P.data + q), vget(__ldg(P.indices + q)), a);
             a += __shfl_xor_sync(FULL, a, 4);
             a += __shfl_xor_sync(FULL, a, 2);
             a += __shfl_xor_sync(FULL, a, 1);
@@ -459,7 +600,25 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
             const double got = __shfl_sync(FULL, a, (lane & 3) * 8);
             if ((lane >> 2) == b) cval = got;
         }
-        if (valid) epilogue(i, j, cval, nrm, bj);
+        if (mt.valid) epilogue(rd * 32 + lane, mt.j, cval, mt.nrm, mt.bj);
+    };
+    const int64_t r0 = (int64_t)g.c * W + w;
+    if (r0 >= nround) return;
+    Buf A, B;
+    Meta m0 = load_meta(r0), m1 = load_meta(r0 + GW);
+    load_buf(m0, A);
+    for (int64_t rd = r0; rd < nround; rd += 2 * GW) {
+        // even round: values in A; fetch the odd round into B
+        Meta m2 = load_meta(rd + 2 * GW);
+        if (rd + GW < nround) load_buf(m1, B);
+        reduce_buf(rd, m0, A);
+        if (rd + GW >= nround) break;
+        // odd round: values in B; fetch the next even round into A
+        Meta m3 = load_meta(rd + 3 * GW);
+        if (rd + 2 * GW < nround) load_buf(m2, A);
+        reduce_buf(rd + GW, m1, B);
+        m0 = m2;
+        m1 = m3;
     }
 }
 
@@ -470,13 +629,40 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
                            int* tile_valid = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = P.n;
-    const bool wide = !P.sparse && P.gemv_wide && stg != nullptr && (int64_t)P.smem_total >= 2 * P.ld * (int64_t)sizeof(T);
+    const bool wide = !P.sparse && P.gemv_wide && stg != nullptr &&
+                      (int64_t)P.smem_total >= 2 * P.ld * (int64_t)sizeof(T) + kWidePartBytes;
     const bool stage = n <= P.vs_cap && !wide;
     if (stage) {
-        for (int r = threadIdx.x; r < n + 2; r += blockDim.x) vs[r] = r < n ? v[r] : 0.0;
+        if (n >= 2048 && (n & 1) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+            // long centre vector (cfg3: 160 KB): one TMA bulk copy per 32 KB instead of 8-byte loads
+            __shared__ unsigned long long s_vbar;
+            const unsigned vb = smem_u32(&s_vbar);
+            __syncthreads();                     // earlier readers of vs are done before the async-proxy writes
+            if (threadIdx.x == 0) {
+                mbar_init(&s_vbar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx_s(vb, (unsigned)(n * 8));
+                for (int off = 0; off < n; off += 4096) {
+                    const int cnt = min(4096, n - off);
+                    tma_bulk_g2s_s(smem_u32(vs + off), v + off, (unsigned)(cnt * 8), vb);
+                }
+                vs[n] = 0.0; vs[n + 1] = 0.0;
+            }
+            __syncthreads();
+            if (!mbar_test_s(vb, 0)) {
+                const unsigned long long t0 = gtimer();
+                while (!mbar_test_s(vb, 0)) spin_guard(t0, 7, n, 0, 0, 0);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(vb) : "memory");
+        } else {
+            for (int r = threadIdx.x; r < n + 2; r += blockDim.x) vs[r] = r < n ? v[r] : 0.0;
+        }
         __syncthreads();
     }
     const double* vv = stage ? vs : v;
+    const unsigned vs_s = stage ? smem_u32(vs) : 0u;
     double bmax = -1.0;
     int64_t barg = INT64_MAX;
     const int64_t GW = (int64_t)g.G * W;
@@ -497,7 +683,7 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
         }
     };
     if (P.sparse && P.csc_short) {
-        group_gemv_csc_short(g, P, vv, cols, m, mode, epilogue);
+        group_gemv_csc_short(g, P, vv, stage, cols, m, mode, epilogue);
     } else if (wide) {
         // vs is not staged in this mode: the ring takes the whole dynamic shared memory
         group_gemv_wide<T>(g, P, v, cols, m, mode, stg, (int64_t)P.smem_total, epilogue);
@@ -535,6 +721,7 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
+        const unsigned long long pol_stream = l2_policy_evict_first();
         auto issue = [&](int k) {           // warp 0: stage k into slot k % kGStages
             const int s = k % kGStages;
             const int64_t i0 = lo + (int64_t)k * C, i1 = min(hi, i0 + C);
@@ -543,11 +730,12 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             if (lane == 0) mbar_expect_tx_s(b, (unsigned)((i1 - i0) * colb));
             __syncwarp();
             if (!cols) {
-                if (lane == 0) tma_bulk_g2s_s(dst, X + i0 * P.ld, (unsigned)((i1 - i0) * colb), b);
+                if (lane == 0) tma_bulk_g2s_hint(dst, X + i0 * P.ld, (unsigned)((i1 - i0) * colb), b, pol_stream);
             } else {
                 // one column per lane: the gathered indices load in parallel
                 for (int64_t i = i0 + lane; i < i1; i += 32)
-                    tma_bulk_g2s_s(dst + (unsigned)((i - i0) * colb), X + (int64_t)cols[i] * P.ld, (unsigned)colb, b);
+                    tma_bulk_g2s_hint(dst + (unsigned)((i - i0) * colb), X + (int64_t)cols[i] * P.ld, (unsigned)colb, b,
+                                      pol_stream);
             }
         };
         if (w == 0)
@@ -582,7 +770,8 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             const T* base = reinterpret_cast<const T*>(stg + (size_t)s * sb);
             for (int l = 0; w + l * W < cn; ++l) {
                 const int cc = w + l * W;
-                const double cval = ColDotS<T>::run(base + (int64_t)cc * P.ld, vv, n, lane);
+                const double cval = stage ? ColDotSS<T>::run(stg0 + (unsigned)(s * sb) + (unsigned)(cc * colb), vs_s, n, lane)
+                                          : ColDotS<T>::run(base + (int64_t)cc * P.ld, vv, n, lane);
                 const int64_t j = __shfl_sync(0xffffffffu, jc, l);
                 const double nrm = __shfl_sync(0xffffffffu, nc, l);
                 const double bj = __shfl_sync(0xffffffffu, bc, l);
@@ -1763,7 +1952,7 @@ __host__ __device__ inline size_t cd_csc_smem_bytes(int64_t n) {
     return (a + 15) / 16 * 16 + (size_t)kSpMW * sizeof(SpMember);
 }
 
-static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m64, unsigned char* smem) {
+static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m64, unsigned char* smem, int64_t lo64 = 0) {
     SolveCtl* ctl = P.ctl;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
     const int n = P.n, m = (int)m64;
@@ -1781,7 +1970,7 @@ static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m64,
     const double rho0 = ctl->anchor_norm;
     for (int r = tid; r < n; r += blockDim.x) srho[r] = P.rho[r];
     for (int k = tid; k < nbw; k += blockDim.x) bm[k] = 0u;
-    if (tid == 0) { s_D = use_t ? ctl->cd_delta : 0.0; s_a = 0; s_tb = 0; s_tend = 0; }
+    if (tid == 0) { s_D = use_t ? ctl->cd_delta : 0.0; s_a = (int)lo64; s_tb = 0; s_tend = 0; }
     double gstep = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * lam;     // warp 0's copy
     long long n_unc = 0, n_nz = 0, n_roll = 0, n_mem = 0;                 // warp 0 lane 0
     __syncthreads();
@@ -2014,7 +2203,7 @@ static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m64,
         ctl->epoch_nz = n_nz;
         ctl->n_requeue += n_roll;
         ctl->n_cand += n_mem;
-        P.sc->visits += (unsigned long long)m;
+        P.sc->visits += (unsigned long long)(m - (int)lo64);
         P.sc->uncertified += (unsigned long long)n_unc;
         P.sc->nonzero += (unsigned long long)n_nz;
     }
@@ -2040,7 +2229,7 @@ static __device__ __noinline__ void cd_epoch_csc(const SolveDev& P, int64_t m64,
 // Accepted nonzero members have pairwise disjoint rows, so their axpys are
 // applied in parallel -- the arithmetic is the sequential CD's, bit for bit.
 // The certification cut-off and the statistics are those of cd_epoch_csc.
-static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t m64, unsigned char* smem) {
+static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t m64, unsigned char* smem, int64_t lo64 = 0) {
     SolveCtl* ctl = P.ctl;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
     const int n = P.n, m = (int)m64;
@@ -2059,7 +2248,7 @@ static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t 
     const double lam = P.lam;
     const double rho0 = ctl->anchor_norm;
     for (int r = tid; r < n; r += blockDim.x) srho[r] = P.rho[r];
-    if (tid == 0) { s_D = use_t ? ctl->cd_delta : 0.0; s_a = 0; s_tb = 0; s_tend = 0; }
+    if (tid == 0) { s_D = use_t ? ctl->cd_delta : 0.0; s_a = (int)lo64; s_tb = 0; s_tend = 0; }
     double gstep = ctl->cd_gstep > 0.0 ? ctl->cd_gstep : 1e-2 * lam;
     long long n_unc = 0, n_nz = 0, n_roll = 0, n_mem = 0;
     __syncthreads();
@@ -2291,7 +2480,7 @@ static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t 
         ctl->epoch_nz = n_nz;
         ctl->n_requeue += n_roll;
         ctl->n_cand += n_mem;
-        P.sc->visits += (unsigned long long)m;
+        P.sc->visits += (unsigned long long)(m - (int)lo64);
         P.sc->uncertified += (unsigned long long)n_unc;
         P.sc->nonzero += (unsigned long long)n_nz;
     }
@@ -2311,11 +2500,11 @@ static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t 
 #include "gs_cd_blk.cuh"
 namespace gs {
 
-// dense CD epoch: blocked chain (cd_gram == 2, R <= 4) or the ring consumers
+// dense CD epoch: blocked chain (cd_gram == 2, R <= 5) or the ring consumers
 template <typename T, int R>
 static __device__ __forceinline__ void cd_epoch_dense_any(const SolveDev& P, int64_t m, unsigned char* smem,
                                                           int* tile_valid) {
-    if constexpr (R <= 4) {
+    if constexpr (R <= 5) {
         if (P.cd_gram == 2) { cd_epoch_blk<T, R>(P, m, P.cd_warps, smem, tile_valid); return; }
     }
     cd_epoch_dense<T, R>(P, m, P.cd_warps, smem, tile_valid);
@@ -2600,6 +2789,41 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
         }
         // ---- one CD epoch over the active set ----
         const int64_t m = sc->m;
+        // Sparse designs: the epoch runs in position chunks, each re-anchored (c_i, t_i
+        // from the current rho, Delta = 0) by the whole group just before CTA 0 walks it.
+        // The norm-based drift bound is far too pessimistic for 20-nonzero columns once
+        // a few hundred updates have accumulated; with the drift restarted per chunk the
+        // uncertified visits fall to about the support (exact skips only, so the
+        // arithmetic is unchanged).  One pass over X_A per epoch in total.
+        const int nch = (P.sparse && P.certify && P.cd_chunk_pos > 0 && m > 0)
+                            ? (int)imin64(256, imax64(1, (m + P.cd_chunk_pos - 1) / P.cd_chunk_pos)) : 1;
+        if (nch > 1) {
+            int64_t unc = 0, nz = 0;
+            for (int ch = 0; ch < nch; ++ch) {
+                const int64_t c0 = m * ch / nch, c1 = m * (ch + 1) / nch;
+                const unsigned long long tr0 = gtimer();
+                const double anchor = sc->rho_norm_ub;
+                group_gemv<T>(g, P, P.rho, P.A + c0, c1 - c0, G_CERT, P.c + c0, P.t + c0, anchor, gam, 0.0, vs, smem, 0, &s_tile_valid);
+                if (g.c == 0 && threadIdx.x == 0) { ctl->anchor_norm = anchor; ctl->cd_delta = 0.0; ctl->n_refresh++; }
+                group_sync(g);
+                if (g.c == 0) {
+                    const unsigned long long td0 = gtimer();
+                    if (threadIdx.x == 0) ctl->t_refresh += td0 - tr0;
+                    if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, c1, smem, c0); else cd_epoch_csc(P, c1, smem, c0);
+                    if (threadIdx.x == 0) ctl->t_cd += gtimer() - td0;
+                    unc += ctl->epoch_unc; nz += ctl->epoch_nz;
+                }
+                group_sync(g);
+            }
+            if (g.c == 0 && threadIdx.x == 0) {
+                ctl->epoch_unc = unc; ctl->epoch_nz = nz;
+                ctl->passes++;
+                ctl->need_refresh = 0;
+            }
+            group_sync(g);
+            ++k;
+            continue;
+        }
         if (P.certify && ctl->need_refresh && m > 0) {
             const unsigned long long tr0 = gtimer();
             const double anchor = sc->rho_norm_ub;
@@ -2642,9 +2866,20 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
     }
     if (g.c == 0 && threadIdx.x == 0) { ctl->done = 1; ctl->k = k; }
     if (P.cd_prof && g.c == 0 && threadIdx.x == 0 && ctl->n_win)
-        printf("cdprof lam=%.6e windows=%llu members=%llu cyc/win: form=%.0f wait=%.0f red=%.0f chain=%.0f upd=%.0f\n", P.lam,
-               ctl->n_win, ctl->n_mem, (double)ctl->c_form / ctl->n_win, (double)ctl->c_wait / ctl->n_win,
-               (double)ctl->c_red / ctl->n_win, (double)ctl->c_chain / ctl->n_win, (double)ctl->c_upd / ctl->n_win);
+    {
+        const double nw = (double)ctl->n_win;
+        if (P.cd_gram == 2)
+            printf("cdprof lam=%.6e windows=%llu members=%llu cyc/win warp0: wait=%.0f dots=%.0f bar=%.0f chain=%.0f commit=%.0f"
+                   " | warp1: wait=%.0f dots=%.0f bar=%.0f chain=%.0f commit=%.0f | producer: idle=%.0f scan=%.0f issue=%.0f\n",
+                   P.lam, ctl->n_win, ctl->n_mem,
+                   ctl->c_wait / nw, ctl->c_red / nw, ctl->c_upd / nw, ctl->c_chain / nw, ctl->c_form / nw,
+                   ctl->c_w1[0] / nw, ctl->c_w1[1] / nw, ctl->c_w1[2] / nw, ctl->c_w1[3] / nw, ctl->c_w1[4] / nw,
+                   ctl->c_w1[5] / nw, ctl->c_pr[0] / nw, ctl->c_pr[1] / nw);
+        else
+            printf("cdprof lam=%.6e windows=%llu members=%llu cyc/win: form=%.0f wait=%.0f red=%.0f chain=%.0f upd=%.0f\n", P.lam,
+                   ctl->n_win, ctl->n_mem, ctl->c_form / nw, ctl->c_wait / nw, ctl->c_red / nw, ctl->c_chain / nw,
+                   ctl->c_upd / nw);
+    }
     (void)broke;
 }
 

@@ -36,11 +36,6 @@ class DesignMatrix:
     def __init__(self, storage, tail_weight: float = 0.0):
         if tail_weight < 0:
             raise ValueError("tail_weight must be non-negative")
-        if tail_weight > 0 and sp.issparse(storage):
-            # the stored-tail CSC solve of a sparse base is not parity-green yet
-            # (its Elastic-Net KKT check fails on the B200): refused, never silently wrong
-            raise NotImplementedError("Elastic-Net tail over a sparse design is not on the B200 path "
-                                      "in this build (dense designs are)")
         lib = _lib.load()
         handle = ctypes.c_void_p()
         if sp.issparse(storage):
@@ -102,6 +97,81 @@ class DesignMatrix:
                                            self.n_base + self.n_cols, self.n_cols, _lib.f64p(nsq),
                                            ctypes.byref(handle)))
         return handle
+
+    @classmethod
+    def from_device(cls, dev_ptr: int, n: int, p: int, ld: int, dtype) -> "DesignMatrix":
+        """Dense design from a device buffer (column j at ``dev_ptr + j*ld``
+        elements): device-to-device copy, no host storage.  The column-sharded
+        path builds the survivors' sub-design from columns received over NCCL
+        this way; the caller synchronises the producer of
+        the buffer first."""
+        lib = _lib.load()
+        self = cls.__new__(cls)
+        handle = ctypes.c_void_p()
+        dt = _lib.GS_DTYPE_F32 if np.dtype(dtype) == np.float32 else _lib.GS_DTYPE_F64
+        _lib.check(lib.gs_matrix_dense_dev(ctypes.c_void_p(int(dev_ptr)), dt, int(n), int(p), int(ld),
+                                           ctypes.byref(handle)))
+        self._h, self._lib, self._mat = handle, lib, None
+        self.is_sparse = False
+        self.n_base, self.n_cols = int(n), int(p)
+        self.dtype = np.dtype(dtype).type
+        self.tail_weight = 0.0
+        self.tail_scale = 0.0
+        nsq = np.empty(self.n_cols, dtype=np.float64)
+        _lib.check(lib.gs_matrix_norms_sq(self._h, _lib.f64p(nsq)))
+        self._col_norms_sq = nsq
+        self._col_norms = np.sqrt(nsq)
+        return self
+
+    @classmethod
+    def from_blocks(cls, n: int, p: int, dtype, blocks) -> "DesignMatrix":
+        """Dense design uploaded block by block: ``blocks`` yields
+        ``(j0, Xb)`` with ``Xb`` an (n, k) array of the columns j0 .. j0+k.
+        The host never holds more than one block (configs[2] is a 40 GB
+        design); no host copy is kept."""
+        lib = _lib.load()
+        self = cls.__new__(cls)
+        handle = ctypes.c_void_p()
+        npdt = np.dtype(dtype)
+        dt = _lib.GS_DTYPE_F32 if npdt == np.float32 else _lib.GS_DTYPE_F64
+        _lib.check(lib.gs_matrix_dense_alloc(dt, int(n), int(p), ctypes.byref(handle)))
+        self._h, self._lib, self._mat = handle, lib, None
+        for j0, Xb in blocks:
+            Xb = np.asfortranarray(Xb, dtype=npdt)
+            if Xb.shape[0] != n:
+                raise ValueError("block has the wrong number of rows")
+            _lib.check(lib.gs_matrix_dense_set_columns(handle, int(j0), int(Xb.shape[1]),
+                                                       Xb.ctypes.data_as(ctypes.c_void_p), int(n)))
+        _lib.check(lib.gs_matrix_dense_finalize(handle))
+        self.is_sparse = False
+        self.n_base, self.n_cols = int(n), int(p)
+        self.dtype = npdt.type
+        self.tail_weight = 0.0
+        self.tail_scale = 0.0
+        nsq = np.empty(self.n_cols, dtype=np.float64)
+        _lib.check(lib.gs_matrix_norms_sq(self._h, _lib.f64p(nsq)))
+        self._col_norms_sq = nsq
+        self._col_norms = np.sqrt(nsq)
+        return self
+
+    def columns_to_host(self, idx: np.ndarray) -> np.ndarray:
+        """(n, k) host copy of the columns ``idx`` of a dense design (gathered on
+        the device, one D2H copy): the column-subsampled parity checks of
+        designs that have no host copy."""
+        import torch
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        tdt = torch.float32 if self.dtype == np.float32 else torch.float64
+        buf = torch.empty((max(1, idx.size), self.n_base), dtype=tdt, device="cuda")
+        if idx.size:
+            self.gather_columns_to_device(idx, buf.data_ptr(), self.n_base)
+        return np.asfortranarray(buf[: idx.size].cpu().numpy().T)
+
+    def gather_columns_to_device(self, idx: np.ndarray, dst_ptr: int, ld_dst: int) -> None:
+        """Columns ``idx`` into the device buffer at ``dst_ptr`` (``ld_dst``
+        elements per column): the send buffer of the X_A gather."""
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        _lib.check(self._lib.gs_matrix_gather_columns_dev(self._h, _lib.i64p(idx), idx.size,
+                                                          ctypes.c_void_p(int(dst_ptr)), int(ld_dst)))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -226,6 +296,8 @@ class DesignMatrix:
 
     # ------------------------------------------------------------------
     def toarray(self) -> np.ndarray:
+        if self._mat is None:
+            raise ValueError("this design was built from device memory and keeps no host copy")
         base = self._mat.toarray() if self.is_sparse else np.array(self._mat, dtype=np.float64)
         if self.tail_scale > 0.0:                               # design_matrix.py:177-183
             return np.asfortranarray(np.vstack([base, self.tail_scale * np.eye(self.n_cols)]))

@@ -40,12 +40,18 @@ from .solver import Rule, SolverConfig, SolverState
 
 
 class DeviceBackend:
-    """Per-rank compute on the B200: the local column block lives in HBM."""
+    """Per-rank compute on the B200: the local column block lives in HBM.
+
+    The survivors' columns never visit the host: ``columns`` gathers them into
+    a CUDA tensor (the NCCL send buffer) with a device kernel, and
+    ``solve_sub`` builds rank 0's sub-design from the received tensor with a
+    device-to-device copy (``DesignMatrix.from_device``)."""
 
     def __init__(self, X_block, y):
         from .design_matrix import DesignMatrix
-        self.Xh = X_block
-        self.X = DesignMatrix(X_block)
+        self.X = X_block if isinstance(X_block, DesignMatrix) else DesignMatrix(X_block)
+        if self.X.is_sparse:
+            raise NotImplementedError("the column-sharded path gathers dense columns")
         self.y = np.ascontiguousarray(y, dtype=np.float64)
 
     @property
@@ -59,18 +65,31 @@ class DeviceBackend:
         return screen(Sphere(center=np.ascontiguousarray(center, dtype=np.float64), radius=float(radius)),
                       self.X, tol).active_set
 
-    def columns(self, idx) -> np.ndarray:
-        return np.asfortranarray(self.Xh[:, idx])
+    def columns(self, idx):
+        """(k, n) tensor of the local columns ``idx`` on this rank's GPU."""
+        import torch
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        n = self.X.n_base
+        tdt = torch.float32 if self.X.dtype == np.float32 else torch.float64
+        buf = torch.empty((max(1, idx.size), n), dtype=tdt, device=torch.device("cuda", torch.cuda.current_device()))
+        if idx.size:
+            self.X.gather_columns_to_device(idx, buf.data_ptr(), n)
+        return buf[: idx.size]
 
     def solve_sub(self, XA, lam, lambda_max, warm_beta, config):
         """solve(prob, config, warm_beta, active0=all) on the gathered design
-        with the full path's lambda_max (no shortcut below it)."""
+        (a (k, n) CUDA tensor) with the full path's lambda_max (no shortcut
+        below it)."""
+        import torch
         from .design_matrix import DesignMatrix
         from .solver import DeviceSolver
-        dev = DeviceSolver(DesignMatrix(XA), self.y)
+        k, n = int(XA.shape[0]), int(XA.shape[1])
+        torch.cuda.synchronize()              # the gather (NCCL stream) has written XA
+        D_A = DesignMatrix.from_device(XA.data_ptr(), n, k, n, np.float32 if XA.dtype == torch.float32 else np.float64)
+        dev = DeviceSolver(D_A, self.y)
         dev.set_lambda_max(lambda_max)
         dev.set_beta(warm_beta)
-        return dev.solve(lam, config, active0=np.arange(XA.shape[1], dtype=np.int64), active0_mode=1)
+        return dev.solve(lam, config, active0=np.arange(k, dtype=np.int64), active0_mode=1)
 
 
 def _bcast_array(a, src: int = 0):
@@ -98,24 +117,54 @@ def _gather_int(x: np.ndarray, world: int) -> list[np.ndarray]:
     return [o[:c].cpu().numpy() for o, c in zip(outs, cnts)]
 
 
-def _gather_columns(cols: np.ndarray, n: int, world: int, rank: int):
-    """Gather every rank's (n x k_g) column block to rank 0, in rank order."""
+def _gather_columns(cols, n: int, world: int, rank: int):
+    """Gather every rank's (k_g, n) column tensor to rank 0, in rank order.
+    The tensors stay on the communication device (GPU memory under NCCL: the
+    transfer is device to device over NVLink); rank 0 gets the (sum k_g, n)
+    tensor, the others None."""
     import torch
     import torch.distributed as dist
-    dev = D._device()
-    k = cols.shape[1]
+    k = int(cols.shape[0])
     ks = _gather_int(np.array([k], dtype=np.int64), world)
     ks = [int(a[0]) for a in ks]
     mx = max(1, max(ks))
-    buf = torch.zeros((mx, n), dtype=torch.float64 if cols.dtype == np.float64 else torch.float32, device=dev)
+    # under NCCL the buffers are the GPU tensors themselves; only the gloo
+    # fallback of the 1-GPU test box (ranks sharing a device) stages on the host
+    comm = D._device()
+    buf = torch.zeros((mx, n), dtype=cols.dtype, device=comm)
     if k:
-        buf[:k] = torch.as_tensor(np.ascontiguousarray(cols.T))
+        buf[:k] = cols
     outs = [torch.zeros_like(buf) for _ in range(world)] if rank == 0 else None
     dist.gather(buf, outs, dst=0)
     if rank != 0:
         return None
-    parts = [o[:kk].cpu().numpy() for o, kk in zip(outs, ks)]
-    return np.asfortranarray(np.concatenate(parts, axis=0).T)
+    return torch.cat([o[:kk] for o, kk in zip(outs, ks)], dim=0).to(cols.device)
+
+
+_ST_OK, _ST_INFEASIBLE, _ST_NUMERICAL, _ST_OTHER = 0, 1, 2, 3
+
+
+def _sync_status(exc: BaseException | None, src: int = 0) -> None:
+    """Rank ``src`` reports the exception it caught (or None); every rank
+    learns the status word and raises together, so no rank is left blocked in
+    the next collective when the reference's synchronous errors
+    (InfeasibleDualError / NumericalInconsistencyError, solver.py:219-221)
+    fire on rank 0."""
+    import torch.distributed as dist
+    code = _ST_OK
+    if exc is not None:
+        code = (_ST_INFEASIBLE if isinstance(exc, InfeasibleDualError)
+                else _ST_NUMERICAL if isinstance(exc, NumericalInconsistencyError) else _ST_OTHER)
+    code = int(_bcast_array([float(code)], src)[0])
+    if code == _ST_OK:
+        return
+    if exc is not None and dist.get_rank() == src:
+        raise exc
+    if code == _ST_INFEASIBLE:
+        raise InfeasibleDualError(f"dual point infeasible on rank {src}")
+    if code == _ST_NUMERICAL:
+        raise NumericalInconsistencyError(f"numerical inconsistency reported by rank {src}")
+    raise RuntimeError(f"rank {src} failed; see its traceback")
 
 
 def run_path_sharded(backend, y: np.ndarray, grid: np.ndarray, config: SolverConfig, p_total: int,
@@ -172,18 +221,23 @@ def run_path_sharded(backend, y: np.ndarray, grid: np.ndarray, config: SolverCon
             if seq:
                 # G_t = P_t(beta_prev) - D_t(theta_prev) with rho_prev (problem.py:57-86)
                 hdr = np.zeros(n + 1)
+                err = None
                 if rank == 0:
-                    beta_p, th_p, rho_p = prev
-                    if th_p.feasibility_margin < -1e-9:
-                        raise InfeasibleDualError(f"dual point infeasible: margin={th_p.feasibility_margin}")
-                    primal = 0.5 * float(np.dot(rho_p, rho_p)) + lam * float(np.sum(np.abs(beta_p)))
-                    diff = th_p.theta - y / lam
-                    dual = 0.5 * y_norm_sq - 0.5 * lam ** 2 * float(np.dot(diff, diff))
-                    gap = primal - dual
-                    if gap < -1e-10:
-                        raise NumericalInconsistencyError(f"negative duality gap beyond tolerance: {gap}")
-                    hdr[:n] = th_p.theta
-                    hdr[n] = float(np.sqrt(2.0 * max(gap, 0.0)) / lam)
+                    try:
+                        beta_p, th_p, rho_p = prev
+                        if th_p.feasibility_margin < -1e-9:
+                            raise InfeasibleDualError(f"dual point infeasible: margin={th_p.feasibility_margin}")
+                        primal = 0.5 * float(np.dot(rho_p, rho_p)) + lam * float(np.sum(np.abs(beta_p)))
+                        diff = th_p.theta - y / lam
+                        dual = 0.5 * y_norm_sq - 0.5 * lam ** 2 * float(np.dot(diff, diff))
+                        gap = primal - dual
+                        if gap < -1e-10:
+                            raise NumericalInconsistencyError(f"negative duality gap beyond tolerance: {gap}")
+                        hdr[:n] = th_p.theta
+                        hdr[n] = float(np.sqrt(2.0 * max(gap, 0.0)) / lam)
+                    except Exception as e:       # reported to every rank below
+                        err = e
+                _sync_status(err)
                 hdr = _bcast_array(hdr)
                 loc = backend.screen(hdr[:n], hdr[n])
             else:
@@ -191,9 +245,15 @@ def run_path_sharded(backend, y: np.ndarray, grid: np.ndarray, config: SolverCon
             glob = _gather_int(col_lo + loc.astype(np.int64), world)
             act = np.concatenate(glob)
             XA = _gather_columns(backend.columns(loc), n, world, rank)
+            err = None
             if rank == 0:
-                beta_full = prev[0] if prev is not None else np.zeros(p_total)
-                bA, cert, st = backend.solve_sub(XA, float(lam), lmax, beta_full[act], config)
+                try:
+                    beta_full = prev[0] if prev is not None else np.zeros(p_total)
+                    bA, cert, st = backend.solve_sub(XA, float(lam), lmax, beta_full[act], config)
+                except Exception as e:
+                    err = e
+            _sync_status(err)
+            if rank == 0:
                 beta = np.zeros(p_total)
                 beta[act] = bA
                 state = SolverState(beta=beta, residual=st.residual, active=act[st.active], theta=st.theta,

@@ -113,6 +113,51 @@ def cfg2(p=1_000_000, n=10_000, k=500, block=10_000):
                               storage="dense-f32"))
 
 
+def cfg2_block(b: int, n: int = 10_000, block: int = 10_000, width: int | None = None) -> np.ndarray:
+    """Columns [b*block, b*block + width) of the cfg2 design: i.i.d. N(0,1)
+    float32 draws of ``default_rng([2, b])``, unit norm (float64 norms),
+    stored float32, F-ordered (n, width) -- exactly ``cfg2``'s block b."""
+    width = block if width is None else width
+    Z = np.random.default_rng([2, b]).standard_normal((width, n), dtype=np.float32)
+    Zd = Z.astype(np.float64)
+    Zd /= np.sqrt(np.einsum("ij,ij->i", Zd, Zd))[:, None]
+    return np.asfortranarray(Zd.T.astype(np.float32))
+
+
+def cfg2_streamed(p=1_000_000, n=10_000, k=500, block=10_000, col_range=None, on_block=None):
+    """configs[2] without ever holding the 40 GB design on the host: the
+    blocks of ``cfg2`` are generated one at a time; the response is
+    y = sum_blocks X_b beta*_b + noise with the block signals accumulated in
+    float64 in block order (``cfg2`` itself multiplies the whole matrix at
+    once, so the two responses agree to round-off, not bit for bit: this is
+    its own seeded instance family, used for the full-size and the
+    column-sharded runs).  Returns (X_shard, y, beta*, meta): ``X_shard`` holds
+    the columns ``col_range`` (default: none, pass ``on_block(b0, Xb)`` to
+    consume the blocks instead, e.g. to upload them)."""
+    rng = np.random.default_rng(2)
+    beta = _support(rng, p, min(k, p), "pm1")
+    lo, hi = (0, 0) if col_range is None else col_range
+    Xs = np.empty((n, hi - lo), dtype=np.float32, order="F") if hi > lo else None
+    signal = np.zeros(n)
+    for b0 in range(0, p, block):
+        b1 = min(p, b0 + block)
+        Xb = cfg2_block(b0 // block, n, block, b1 - b0)
+        nzb = np.flatnonzero(beta[b0:b1])
+        if nzb.size:
+            signal += Xb[:, nzb].astype(np.float64) @ beta[b0:b1][nzb]
+        if hi > lo and b1 > lo and b0 < hi:
+            a, z = max(b0, lo), min(b1, hi)
+            Xs[:, a - lo:z - lo] = Xb[:, a - b0:z - b0]
+        if on_block is not None:
+            on_block(b0, Xb)
+    noise = rng.standard_normal(n)
+    noise *= np.linalg.norm(signal) / (3.0 * np.linalg.norm(noise))
+    y = signal + noise
+    meta = dict(n=n, p=p, k=min(k, p), values="pm1", snr=3.0, block=block,
+                response="block-accumulated signal (cfg2_streamed)", storage="dense-f32")
+    return Xs, y, beta, meta
+
+
 def cfg3(p=1_000_000, n=20_000, nnz_per_col=20):
     """configs[3]: CSC n x p, exactly ``nnz_per_col`` rows per column drawn
     uniformly without replacement, lognormal(0,1) values, unit column norms,

@@ -76,3 +76,59 @@ def test_gloo_world2_reductions():
         assert res[r]["argmax"] == res[r]["argmax_ref"]
         assert res[r]["argmax"][1] == 17
         assert res[r]["sum"] == 0.1 + 0.2
+
+
+def test_bench_reference_arm_under_torchrun_world2():
+    """bench.py's N > 1 launch path on CPU: ``--gpus 2`` relaunches the script
+    as two ranks (torch.distributed.run, 127.0.0.1); rank 0 alone runs the
+    reference arm and prints ONE JSON line, rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--config", "cfg0", "--p", "300", "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["steps"] == 1
+    assert line["config"]["workload"] == "cfg0" and line["config"]["p"] == 300
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_bench_cfg4_problem_sharded_two_ranks():
+    """bench.py --config cfg4 --gpus 2 on the device: problems sharded by index
+    over two ranks (sharing the GPU when the box has one; no kernel of one rank
+    waits on the other), one JSON line with the parity block green."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "cfg4", "--gpus", "2",
+                          "--problems", "4", "--p", "2000", "--steps", "1", "--quick", "--cpu-budget", "5"],
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["config"]["workload"] == "cfg4" and line["scaling"] == "strong"
+    assert line["parity"]["ok"] and line["gpu_launches"] >= 1
+
+
+@pytest.mark.gpu
+def test_bench_cfg2_column_sharded_two_ranks():
+    """bench.py --config cfg2 --gpus 2 on the device: column shards, X_A gathered
+    device to device (gloo moves it when the ranks share one GPU)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "cfg2", "--gpus", "2",
+                          "--p", "20000", "--steps", "1", "--quick"],
+                         capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["path"]["converged"] == 50

@@ -337,9 +337,7 @@ def test_tail_behaves_like_stacked_identity():
     rng = np.random.default_rng(4)
     base = rng.standard_normal((6, 4))
     w = 0.7
-    with pytest.raises(NotImplementedError):
-        gs.DesignMatrix(sp.csc_matrix(base), tail_weight=w)
-    for storage in (base,):
+    for storage in (base, sp.csc_matrix(base)):
         X = gs.DesignMatrix(storage, tail_weight=w)
         explicit = np.vstack([base, np.sqrt(w) * np.eye(4)])
         assert X.n_rows == 10 and X.tail_scale == float(np.sqrt(w))
@@ -369,7 +367,7 @@ def _stacked_oracle(Xh, y, tail):
     return Xo, np.concatenate([y, np.zeros(p)])
 
 
-@pytest.mark.parametrize("alpha,sparse", [(0.5, False), (0.7, False)])
+@pytest.mark.parametrize("alpha,sparse", [(0.5, False), (0.3, True), (0.7, False)])
 def test_elastic_net_tail_matches_oracle(alpha, sparse):
     """F2: to_lasso with a tail (elastic_net.py:34-46) solved on the device
     against the oracle on the stacked design, and the Elastic-Net KKT

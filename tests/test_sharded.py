@@ -50,10 +50,12 @@ class OracleBackend:
         return O.screen(O.Sphere(center=center, radius=float(radius)), self.X, tol).active_set
 
     def columns(self, idx):
-        return np.asfortranarray(self.Xh[:, idx])
+        # (k, n) tensor on the communication device, like DeviceBackend.columns
+        return torch.from_numpy(np.ascontiguousarray(self.Xh[:, idx].T))
 
     def solve_sub(self, XA, lam, lambda_max, warm_beta, config):
         O = self.O
+        XA = np.asfortranarray(XA.numpy().T)
         prob = O.LassoProblem(O.DesignMatrix(XA), self.y, lam, lambda_max=(lambda_max, 0))
         ocfg = O.SolverConfig(epsilon=config.epsilon, max_passes=config.max_passes,
                               screen_every=config.screen_every, rule=config.rule.value)
