@@ -537,7 +537,7 @@ def main():
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--ref-budget", type=float, default=900.0,
+    ap.add_argument("--ref-budget", type=float, default=600.0,
                     help="reference arm: stop starting new full paths after this many seconds")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--p", type=int, default=None, help="column count override (cfg2 / cfg4 prefixes)")

@@ -28,7 +28,7 @@
 //   3. the coordinate chain in registers, every lane of every warp
 //      redundantly (no broadcast of the d's is needed afterwards), branch-free:
 //         g_b = h_b - sum_{c<b} d_c G(b,c)   (folded in as the d's appear)
-//         z = beta_b + RN(g_b/nsq_b); soft threshold; d_b
+//         z = fl(beta_b + g_b RN(1/nsq_b)); soft threshold; d_b
 //      then the running drift bound D over the members (round-up adds);
 //   4. the first member after which D > Dp ends the window there (the gap
 //      after it may hold a position that lost its certificate): members up
@@ -222,7 +222,7 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             __syncwarp();
             if (lane < found) {
                 tma_bulk_g2s_hint(cols_s + (unsigned)slot * slot_bytes + (unsigned)lane * cbytes, X + (int64_t)mj * P.ld,
-                                  cbytes, bb, pol_keep);
+                                  cbytes, bb, pol_keep, P.l2_hint);
                 tma_bulk_g2s_s(smem_u32(&bc->info[islot][lane]), P.cinfo + mj, (unsigned)sizeof(ColInfo), bb);
             }
             if (last) emitted_last = true;
@@ -233,6 +233,10 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
     } else if (w < NW) {
         // ================= compute warps =================
         const double rho0 = ctl->anchor_norm;
+        // P lives in global memory: the pointers the commit needs, read once
+        double* const p_beta = P.beta;
+        ColInfo* const p_cinfo = P.cinfo;
+        float* const p_t = P.t;
         double D = D0;
         double gstep = gstep0;
         double rr[R];
@@ -332,23 +336,24 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             for (int i = 0; i < kBW * (kBW - 1) / 2; ++i) Gs[i] = __shfl_sync(FULL, tot, kBW + i);
             const ColInfo* inf = &bc->info[i3][0];
             // the members' constants first (one round of shared-memory loads), then the pure chain
-            double c_ns[kBW], c_iv[kBW], c_u[kBW], c_bj[kBW];
+            double c_iv[kBW], c_u[kBW], c_bj[kBW];
 #pragma unroll
             for (int b = 0; b < kBW; ++b) {
-                const double2 nsiv = *reinterpret_cast<const double2*>(&inf[b].ns);     // ns, inv
-                c_ns[b] = nsiv.x; c_iv[b] = nsiv.y;
+                c_iv[b] = inf[b].inv;
                 c_u[b] = inf[b].u;
                 c_bj[b] = inf[b].beta;
             }
+            // z = fl(beta + g * RN(1/nsq)): one FMA on the serial path instead of the
+            // correctly rounded quotient (three dependent operations).  The Gram form of g
+            // already differs from the stored-residual dot by a few ulps, so the quotient's
+            // last bit is not what parity rests on; the certified skips stay exact because
+            // cert_threshold certifies against lam (1 - 1e-15) (gs_kernels.cuh).
 #pragma unroll
             for (int b = 0; b < kBW; ++b) {
-                const double g = acc[b];
-                const double q0 = g * c_iv[b];
-                const double rq = fma(-q0, c_ns[b], g);
-                const double qq = fma(rq, c_iv[b], q0);             // RN(g / nsq)
-                const double z = c_bj[b] + qq;
+                const double z = fma(acc[b], c_iv[b], c_bj[b]);
                 const double uq = c_u[b];
-                const double nb = z > uq ? z - uq : (z < -uq ? z + uq : 0.0);
+                const double zp = z - uq, zm = z + uq;
+                const double nb = z > uq ? zp : (z < -uq ? zm : 0.0);
                 const double d = (b < cnt) ? nb - c_bj[b] : 0.0;
 #pragma unroll
                 for (int c = b + 1; c < kBW; ++c) acc[c] = fma(-d, Gs[c * (c - 1) / 2 + b], acc[c]);
@@ -397,10 +402,10 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             if (w == 0 && lane < ncommit && dmine != 0.0) {
                 // lane b commits member b (values of its own chain copy)
                 const int j = dsc->j[lane], pos = dsc->pos[lane];
-                P.beta[j] = nbmine;
-                P.cinfo[j].beta = nbmine;
+                p_beta[j] = nbmine;
+                p_cinfo[j].beta = nbmine;
                 if (use_t && inf[lane].beta == 0.0) {
-                    P.t[pos] = -1.0f;                                  // now in the support
+                    p_t[pos] = -1.0f;                                  // now in the support
                     if (m <= kBTile) ts[pos] = -1.0f;                  // resident tile (positions 0 .. m)
                 }
             }

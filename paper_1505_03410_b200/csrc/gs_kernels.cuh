@@ -285,7 +285,10 @@ struct GemvArgs {
 __device__ __forceinline__ double cert_threshold(double c, double norm, double lam,
                                                  double rho0, double gam) {
     const double k = 1.0 + 4.0 * gam + 1e-13;
-    const double num = __dsub_rd(__dsub_rd(lam, fabs(c)), __dmul_ru(__dmul_ru(2.0 * k, gam), __dmul_ru(norm, rho0)));
+    // certified against lam (1 - 1e-15): |g| stays a few ulps inside lam, so the blocked
+    // chain's z = fl(g * RN(1/nsq)) (no division) is still within [-u, u] for u = RN(lam/nsq)
+    const double lam_s = __dmul_rd(lam, 1.0 - 1e-15);
+    const double num = __dsub_rd(__dsub_rd(lam_s, fabs(c)), __dmul_ru(__dmul_ru(2.0 * k, gam), __dmul_ru(norm, rho0)));
     const double den = __dmul_ru(norm, __dmul_ru(k, k));
     if (!(num > 0.0)) return -1.0;
     return __ddiv_rd(num, den);

@@ -127,6 +127,8 @@ struct SolveDev {
     int csc_short;       // CSC GEMV: 8 lanes per column (short columns), 32 columns per warp round
     int smem_total;      // dynamic shared memory of the launch (bytes)
     int cd_chunk_pos;    // sparse CD: positions per re-anchored chunk of an epoch (0: whole epoch)
+    int l2_hint;         // TMA copies carry L2 eviction-priority hints (GEMV evict_first, CD columns evict_last)
+    int lds_explicit;    // staged GEMV reads shared memory through ld.shared on 32-bit addresses
 };
 
 struct Group {
@@ -216,7 +218,8 @@ static __device__ __forceinline__ unsigned long long l2_policy_evict_last() {
     return pol;
 }
 static __device__ __forceinline__ void tma_bulk_g2s_hint(unsigned dst, const void* src, unsigned bytes, unsigned b,
-                                                         unsigned long long pol) {
+                                                         unsigned long long pol, int use_hint = 1) {
+    if (!use_hint) { tma_bulk_g2s_s(dst, src, bytes, b); return; }
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(b), "l"(pol) : "memory");
 }
@@ -309,27 +312,27 @@ constexpr int kGStages = 4;     // TMA stages of the staged dense GEMV
 // time) instead of LDS
 static __device__ __forceinline__ double lds_f64(unsigned a) {
     double v;
-    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
 }
 static __device__ __forceinline__ double2 lds_f64x2(unsigned a) {
     double2 v;
-    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
     return v;
 }
 static __device__ __forceinline__ float4 lds_f32x4(unsigned a) {
     float4 v;
-    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
 }
 static __device__ __forceinline__ float lds_f32x1(unsigned a) {
     float v;
-    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
     return v;
 }
 static __device__ __forceinline__ uint4 lds_u32x4(unsigned a) {
     uint4 v;
-    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
 
@@ -439,7 +442,7 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
         const unsigned b = bar0 + 8u * s;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx_s(b, (unsigned)colb);
-        tma_bulk_g2s_hint(stg0 + (unsigned)(s * colb), X + j * P.ld, (unsigned)colb, b, pol_stream);
+        tma_bulk_g2s_hint(stg0 + (unsigned)(s * colb), X + j * P.ld, (unsigned)colb, b, pol_stream, P.l2_hint);
     };
     // epilogues run lane-parallel, one batch of kEB columns at a time, by the warp
     // whose turn it is (batch index mod W): coalesced norm loads and mark stores,
@@ -530,12 +533,12 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
 // between the trips that touch them and re-fetched from L2)
 static __device__ __forceinline__ double ldg_stream_f64(const double* p) {
     double v;
-    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
 static __device__ __forceinline__ int32_t ldg_stream_s32(const int32_t* p) {
     int32_t v;
-    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 
@@ -543,6 +546,13 @@ template <class Epi>
 static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, const SolveDev& P, const double* vv,
                                                             const bool staged, const int32_t* cols, int64_t m, int mode,
                                                             Epi epilogue) {
+    // P lives in global memory: keep its pointers in registers (the loads below would
+    // otherwise re-read them from the descriptor before every access)
+    const double* __restrict__ p_data = P.data;
+    const int32_t* __restrict__ p_indices = P.indices;
+    const int64_t* __restrict__ p_indptr = P.indptr;
+    const double* __restrict__ p_norms = P.norms;
+    const double* p_beta = P.beta;
     const unsigned vs_s = staged ? smem_u32(vv) : 0u;
     auto vget = [&](int32_t r) -> double { return staged ? lds_f64(vs_s + 8u * (unsigned)r) : __ldg(vv + r); };
     constexpr int T3 = 3;                            // unrolled trips of 8 nonzeros
@@ -562,10 +572,10 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
         mt.j = mt.valid ? (cols ? (int64_t)cols[i] : i) : 0;
         mt.plo = 0; mt.phi = 0; mt.nrm = 0.0; mt.bj = 0.0;
         if (mt.valid) {
-            mt.plo = __ldg(P.indptr + mt.j);
-            mt.phi = __ldg(P.indptr + mt.j + 1);
-            mt.nrm = __ldg(P.norms + mt.j);
-            if (mode == G_CERT) mt.bj = P.beta[mt.j];
+            mt.plo = __ldg(p_indptr + mt.j);
+            mt.phi = __ldg(p_indptr + mt.j + 1);
+            mt.nrm = __ldg(p_norms + mt.j);
+            if (mode == G_CERT) mt.bj = p_beta[mt.j];
         }
         return mt;
     };
@@ -580,8 +590,8 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
             for (int t = 0; t < T3; ++t) {
                 const int64_t q = B.qlo[b] + 8 * t;
                 const bool ok = q < B.qhi[b];
-                B.dv[b][t] = ok ? ldg_stream_f64(P.data + q) : 0.0;
-                B.iv[b][t] = ok ? ldg_stream_s32(P.indices + q) : 0;
+                B.dv[b][t] = ok ? ldg_stream_f64(p_data + q) : 0.0;
+                B.iv[b][t] = ok ? ldg_stream_s32(p_indices + q) : 0;
             }
         }
     };
@@ -592,7 +602,7 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
             double a = 0.0;
 #pragma unroll
             for (int t = 0; t < T3; ++t) a = fma(B.dv[b][t], vget(B.iv[b][t]), a);
-            for (int64_t q = B.qlo[b] + 8 * T3; q < B.qhi[b]; q += 8) a = fma(__ldg(P.data + q), vget(__ldg(P.indices + q)), a);
+            for (int64_t q = B.qlo[b] + 8 * T3; q < B.qhi[b]; q += 8) a = fma(__ldg(p_data + q), vget(__ldg(p_indices + q)), a);
             a += __shfl_xor_sync(FULL, a, 4);
             a += __shfl_xor_sync(FULL, a, 2);
             a += __shfl_xor_sync(FULL, a, 1);
@@ -730,12 +740,12 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             if (lane == 0) mbar_expect_tx_s(b, (unsigned)((i1 - i0) * colb));
             __syncwarp();
             if (!cols) {
-                if (lane == 0) tma_bulk_g2s_hint(dst, X + i0 * P.ld, (unsigned)((i1 - i0) * colb), b, pol_stream);
+                if (lane == 0) tma_bulk_g2s_hint(dst, X + i0 * P.ld, (unsigned)((i1 - i0) * colb), b, pol_stream, P.l2_hint);
             } else {
                 // one column per lane: the gathered indices load in parallel
                 for (int64_t i = i0 + lane; i < i1; i += 32)
                     tma_bulk_g2s_hint(dst + (unsigned)((i - i0) * colb), X + (int64_t)cols[i] * P.ld, (unsigned)colb, b,
-                                      pol_stream);
+                                      pol_stream, P.l2_hint);
             }
         };
         if (w == 0)
@@ -770,7 +780,7 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             const T* base = reinterpret_cast<const T*>(stg + (size_t)s * sb);
             for (int l = 0; w + l * W < cn; ++l) {
                 const int cc = w + l * W;
-                const double cval = stage ? ColDotSS<T>::run(stg0 + (unsigned)(s * sb) + (unsigned)(cc * colb), vs_s, n, lane)
+                const double cval = (stage && P.lds_explicit) ? ColDotSS<T>::run(stg0 + (unsigned)(s * sb) + (unsigned)(cc * colb), vs_s, n, lane)
                                           : ColDotS<T>::run(base + (int64_t)cc * P.ld, vv, n, lane);
                 const int64_t j = __shfl_sync(0xffffffffu, jc, l);
                 const double nrm = __shfl_sync(0xffffffffu, nc, l);
