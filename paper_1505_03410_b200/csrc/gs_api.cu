@@ -711,6 +711,8 @@ static void set_plan(const gs_matrix* M, SolveDev& d) {
     d.gemv_wide = gemv_wide_for(M) ? 1 : 0;
     d.csc_short = csc_short_for(M) ? 1 : 0;
     d.smem_total = (int)solve_smem(M);
+    const char* efl = getenv("GS_CSC_FLAT");
+    d.csc_flat = efl ? atoi(efl) : 1;
     const char* el2 = getenv("GS_L2_HINT");
     d.l2_hint = el2 ? atoi(el2) : 1;
     const char* els = getenv("GS_LDS_EXPLICIT");

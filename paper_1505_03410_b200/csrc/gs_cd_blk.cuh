@@ -152,10 +152,16 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
         double Dp = use_t ? __dadd_ru(D0, __dmul_ru(mfac, gstep0)) : 0.0;
         asm volatile("fence.proxy.async.global;" ::: "memory");   // cinfo / beta stores before TMA reads
         const unsigned long long pol_keep = l2_policy_evict_last();   // the chain's columns stay in L2 across GEMV passes
+        // phase cycles (clock64) only in a -DGS_CD_PROFILE build: the counters cost registers,
+        // and this function runs at the 255-register limit
+#ifdef GS_CD_PROFILE
         const bool pprof = P.cd_prof != 0 && lane == 0;
         long long ppc[3] = {0, 0, 0};
         long long ptprev = pprof ? clock64() : 0;
         auto plap = [&](int i) { if (pprof) { const long long t = clock64(); ppc[i] += t - ptprev; ptprev = t; } };
+#else
+        auto plap = [](int) {};
+#endif
         for (;;) {
             // a free column slot (window q - 2 released), a restart request, or the end
             bool stop = false;
@@ -229,7 +235,9 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             ++q;
             plap(2);
         }
+#ifdef GS_CD_PROFILE
         if (pprof) { ctl->c_w1[5] += (unsigned long long)ppc[0]; ctl->c_pr[0] += (unsigned long long)ppc[1]; ctl->c_pr[1] += (unsigned long long)ppc[2]; }
+#endif
     } else if (w < NW) {
         // ================= compute warps =================
         const double rho0 = ctl->anchor_norm;
@@ -245,10 +253,14 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
         int n_unc = 0, n_nz = 0, n_req = 0, gen = 0;
         int k = 0;
         // phase cycles of warp 0 and of a second compute warp, GS_CD_PROF=1
+#ifdef GS_CD_PROFILE
         const bool prof = P.cd_prof != 0 && lane == 0 && (w == 0 || w == 1);
         long long pc[5] = {0, 0, 0, 0, 0};
         long long tprev = prof ? clock64() : 0;
         auto lap = [&](int i) { if (prof) { const long long t = clock64(); pc[i] += t - tprev; tprev = t; } };
+#else
+        auto lap = [](int) {};
+#endif
         for (;;) {
             const int s = k & 1, i3 = k % kBInfo;
             blk_wait(bar_s + 8u * s, k >> 1, 11);
@@ -429,6 +441,7 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             ++k;
         }
         if (tid == 0) st_rel_s(done_s, 1);
+#ifdef GS_CD_PROFILE
         if (prof) {
             if (w == 0) {
                 ctl->c_wait += pc[0]; ctl->c_red += pc[1]; ctl->c_upd += pc[2]; ctl->c_chain += pc[3]; ctl->c_form += pc[4];
@@ -436,6 +449,7 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
                 for (int i = 0; i < 5; ++i) ctl->c_w1[i] += (unsigned long long)pc[i];
             }
         }
+#endif
         // ---- epilogue: rho back, ||rho|| upper bound for the next anchor
         if (NW > 1) named_bar(1, BT);
         double s2 = 0.0;

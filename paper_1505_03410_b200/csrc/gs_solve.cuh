@@ -127,6 +127,7 @@ struct SolveDev {
     int csc_short;       // CSC GEMV: 8 lanes per column (short columns), 32 columns per warp round
     int smem_total;      // dynamic shared memory of the launch (bytes)
     int cd_chunk_pos;    // sparse CD: positions per re-anchored chunk of an epoch (0: whole epoch)
+    int csc_flat;        // CSC full-p pass: flat coalesced loads + products in shared memory
     int l2_hint;         // TMA copies carry L2 eviction-priority hints (GEMV evict_first, CD columns evict_last)
     int lds_explicit;    // staged GEMV reads shared memory through ld.shared on 32-bit addresses
 };
@@ -397,7 +398,7 @@ constexpr int kWideSlots = 8;
 constexpr int kWidePartBytes = 2 * 32 * 8 * 8;     // warp partials of two epilogue batches (tail of the dynamic region)
 
 template <typename T, class Epi>
-static __device__ __forceinline__ void group_gemv_wide(const Group& g, const SolveDev& P, const double* __restrict__ v,
+static __device__ __noinline__ void group_gemv_wide(const Group& g, const SolveDev& P, const double* __restrict__ v,
                                                        const int32_t* cols, int64_t m, int mode, unsigned char* stg,
                                                        int64_t stg_bytes, Epi epilogue) {
     constexpr int E = 16 / (int)sizeof(T);          // elements per 16-byte vector
@@ -411,9 +412,13 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, W = blockDim.x >> 5;
     const int n = P.n;
     const T* X = (const T*)P.X;
-    const int64_t colb = P.ld * (int64_t)sizeof(T);
+    const int64_t ldx = P.ld;
+    const double* __restrict__ p_norms = P.norms;
+    const double* p_beta = P.beta;
+    const int use_hint = P.l2_hint;
+    const int64_t colb = ldx * (int64_t)sizeof(T);
     const int NS = (int)min((int64_t)kWideSlots, (stg_bytes - kWidePartBytes) / colb);
-    const int nvec = (int)(P.ld / E);
+    const int nvec = (int)(ldx / E);
     const int64_t per = (m + g.G - 1) / g.G;
     const int64_t lo = min(m, (int64_t)g.c * per), hi = min(m, lo + per);
     const int nst = (int)(hi - lo);
@@ -442,7 +447,7 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
         const unsigned b = bar0 + 8u * s;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx_s(b, (unsigned)colb);
-        tma_bulk_g2s_hint(stg0 + (unsigned)(s * colb), X + j * P.ld, (unsigned)colb, b, pol_stream, P.l2_hint);
+        tma_bulk_g2s_hint(stg0 + (unsigned)(s * colb), X + j * ldx, (unsigned)colb, b, pol_stream, use_hint);
     };
     // epilogues run lane-parallel, one batch of kEB columns at a time, by the warp
     // whose turn it is (batch index mod W): coalesced norm loads and mark stores,
@@ -452,8 +457,8 @@ static __device__ __forceinline__ void group_gemv_wide(const Group& g, const Sol
             const int k = kb0 + lane;
             const int64_t i = lo + k;
             const int64_t j = cols ? (int64_t)cols[i] : i;
-            const double nrm = __ldg(P.norms + j);
-            const double bj = (mode == G_CERT) ? P.beta[j] : 0.0;
+            const double nrm = __ldg(p_norms + j);
+            const double bj = (mode == G_CERT) ? p_beta[j] : 0.0;
             const double* pp = &s_wpart[(k / kEB) & 1][k % kEB][0];
             double cval = 0.0;
             for (int q = 0; q < W; ++q) cval += pp[q];
@@ -543,7 +548,7 @@ static __device__ __forceinline__ int32_t ldg_stream_s32(const int32_t* p) {
 }
 
 template <class Epi>
-static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, const SolveDev& P, const double* vv,
+static __device__ __noinline__ void group_gemv_csc_short(const Group& g, const SolveDev& P, const double* vv,
                                                             const bool staged, const int32_t* cols, int64_t m, int mode,
                                                             Epi epilogue) {
     // P lives in global memory: keep its pointers in registers (the loads below would
@@ -556,19 +561,21 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
     const unsigned vs_s = staged ? smem_u32(vv) : 0u;
     auto vget = [&](int32_t r) -> double { return staged ? lds_f64(vs_s + 8u * (unsigned)r) : __ldg(vv + r); };
     constexpr int T3 = 3;                            // unrolled trips of 8 nonzeros
+    constexpr int CPR = 16;                          // positions per warp round (two rounds in flight per warp)
+    constexpr int NB = CPR / 4;                      // batches of four columns
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int sub = lane >> 3, sl = lane & 7;
     const int64_t GW = (int64_t)g.G * W;
-    const int64_t nround = (m + 31) / 32;
+    const int64_t nround = (m + CPR - 1) / CPR;
     // software pipeline over this warp's rounds: the column pointers of round
     // r + 2 and the values / row indices of round r + 1 are in flight while
     // round r is reduced (two register buffers, the loop unrolled by two)
     struct Meta { int64_t j, plo, phi; double nrm, bj; bool valid; };
     auto load_meta = [&](int64_t rd) {
         Meta mt;
-        const int64_t i = rd * 32 + lane;
-        mt.valid = rd < nround && i < m;
+        const int64_t i = rd * CPR + lane;
+        mt.valid = rd < nround && lane < CPR && i < m;
         mt.j = mt.valid ? (cols ? (int64_t)cols[i] : i) : 0;
         mt.plo = 0; mt.phi = 0; mt.nrm = 0.0; mt.bj = 0.0;
         if (mt.valid) {
@@ -579,10 +586,10 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
         }
         return mt;
     };
-    struct Buf { double dv[8][T3]; int32_t iv[8][T3]; int64_t qlo[8], qhi[8]; };
+    struct Buf { double dv[NB][T3]; int32_t iv[NB][T3]; int64_t qlo[NB], qhi[NB]; };
     auto load_buf = [&](const Meta& mt, Buf& B) {
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
+        for (int b = 0; b < NB; ++b) {
             const int src = 4 * b + sub;
             B.qlo[b] = __shfl_sync(FULL, mt.plo, src) + sl;
             B.qhi[b] = __shfl_sync(FULL, mt.phi, src);
@@ -598,7 +605,7 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
     auto reduce_buf = [&](int64_t rd, const Meta& mt, const Buf& B) {
         double cval = 0.0;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
+        for (int b = 0; b < NB; ++b) {
             double a = 0.0;
 #pragma unroll
             for (int t = 0; t < T3; ++t) a = fma(B.dv[b][t], vget(B.iv[b][t]), a);
@@ -610,7 +617,7 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
             const double got = __shfl_sync(FULL, a, (lane & 3) * 8);
             if ((lane >> 2) == b) cval = got;
         }
-        if (mt.valid) epilogue(rd * 32 + lane, mt.j, cval, mt.nrm, mt.bj);
+        if (mt.valid) epilogue(rd * CPR + lane, mt.j, cval, mt.nrm, mt.bj);
     };
     const int64_t r0 = (int64_t)g.c * W + w;
     if (r0 >= nround) return;
@@ -632,8 +639,147 @@ static __device__ __forceinline__ void group_gemv_csc_short(const Group& g, cons
     }
 }
 
+// ---------------------------------------------------------------------------
+// Short-column CSC GEMV over CONSECUTIVE columns (the full-p screening pass):
+// flat, fully coalesced loads.  The 8-lane form above asks the memory system
+// for 64-byte (values) and 32-byte (row indices) pieces, four separate ones
+// per load instruction; with ~18 MB of such requests in flight it still
+// delivers only ~1.4 TB/s.  Here a warp round (32 consecutive columns) reads
+// its CONTIGUOUS nonzero range [indptr[c0], indptr[c0+32]) exactly like a
+// copy -- lane l takes entries l, l+32, ... (256-byte and 128-byte requests,
+// every line touched once) -- multiplies each value by its centre entry
+// (gather from the staged centre) and parks the products in a per-warp
+// shared-memory buffer; the columns are then summed out of that buffer by
+// 8-lane groups (conflict-free contiguous reads, three shuffle steps).  The
+// next round's loads are in flight while the current one is reduced.
+// Rounds with more nonzeros than the buffer holds fall back to direct loads.
+// ---------------------------------------------------------------------------
+template <class Epi>
+static __device__ __noinline__ void group_gemv_csc_flat(const Group& g, const SolveDev& P, const double* vv,
+                                                           int64_t m, int mode, double* sbuf_all, int capw, Epi epilogue) {
+    constexpr int CPR = 16;                          // columns per warp round (two rounds in flight per warp:
+                                                     // 32 would need ~170 live registers for the two buffers)
+    constexpr int TU = 10;                           // unrolled trips of 32 entries (320 per round)
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int sub = lane >> 3, sl = lane & 7;
+    const int64_t GW = (int64_t)g.G * W;
+    const int64_t nround = (m + CPR - 1) / CPR;
+    const double* __restrict__ p_data = P.data;
+    const int32_t* __restrict__ p_indices = P.indices;
+    const int64_t* __restrict__ p_indptr = P.indptr;
+    const double* __restrict__ p_norms = P.norms;
+    const double* p_beta = P.beta;
+    const unsigned vs_s = smem_u32(vv);
+    const unsigned sb_s = smem_u32(sbuf_all + (size_t)w * capw);
+    struct Meta { int64_t plo, phi; double nrm, bj; bool valid; };
+    auto load_meta = [&](int64_t rd) {
+        Meta mt;
+        const int64_t j = rd * CPR + lane;
+        mt.valid = rd < nround && lane < CPR && j < m;
+        mt.plo = 0; mt.phi = 0; mt.nrm = 0.0; mt.bj = 0.0;
+        if (mt.valid) {
+            mt.plo = __ldg(p_indptr + j);
+            mt.phi = __ldg(p_indptr + j + 1);
+            mt.nrm = __ldg(p_norms + j);
+            if (mode == G_CERT) mt.bj = p_beta[j];
+        }
+        return mt;
+    };
+    struct Buf { double dv[TU]; int32_t iv[TU]; int64_t qa; int total; };
+    auto load_buf = [&](const Meta& mt, Buf& B) {
+        // the round's nonzero range: first column's start .. last valid column's end
+        const unsigned vmask = __ballot_sync(FULL, mt.valid);
+        const int lastl = 31 - __clz((int)vmask);
+        B.qa = __shfl_sync(FULL, mt.plo, 0);
+        B.total = (int)(__shfl_sync(FULL, mt.phi, lastl < 0 ? 0 : lastl) - B.qa);
+        if (vmask == 0u) B.total = 0;
+        const int lim = B.total <= capw ? B.total : 0;      // oversized rounds load nothing here
+        const double* dbase = p_data + B.qa + lane;         // one 64-bit address per round, immediates per trip
+        const int32_t* ibase = p_indices + B.qa + lane;
+        const int lim_l = lim - lane;
+#pragma unroll
+        for (int t = 0; t < TU; ++t) {
+            const bool ok = 32 * t < lim_l;
+            B.dv[t] = ok ? ldg_stream_f64(dbase + 32 * t) : 0.0;
+            B.iv[t] = ok ? ldg_stream_s32(ibase + 32 * t) : 0;
+        }
+    };
+    auto reduce_buf = [&](int64_t rd, const Meta& mt, const Buf& B) {
+        double cval = 0.0;
+        if (B.total <= capw) {
+            // products into the warp's buffer (entry e at slot e)
+#pragma unroll
+            for (int t = 0; t < TU; ++t) {
+                const int e = 32 * t + lane;
+                if (e < B.total) {
+                    const double pr = B.dv[t] * lds_f64(vs_s + 8u * (unsigned)B.iv[t]);
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(sb_s + 8u * (unsigned)e), "d"(pr) : "memory");
+                }
+            }
+            for (int e = 32 * TU + lane; e < B.total; e += 32) {
+                const double pr = __ldg(p_data + B.qa + e) * lds_f64(vs_s + 8u * (unsigned)__ldg(p_indices + B.qa + e));
+                asm volatile("st.shared.f64 [%0], %1;" ::"r"(sb_s + 8u * (unsigned)e), "d"(pr) : "memory");
+            }
+            __syncwarp();
+#pragma unroll
+            for (int b = 0; b < CPR / 4; ++b) {
+                const int src = 4 * b + sub;
+                const int64_t clo = __shfl_sync(FULL, mt.plo, src), chi = __shfl_sync(FULL, mt.phi, src);
+                const int off = (int)(clo - B.qa), len = (int)(chi - clo);
+                double a = 0.0;
+                const unsigned cb_s = sb_s + 8u * (unsigned)(off + sl);
+                if (sl < len) a = lds_f64(cb_s);
+                if (sl + 8 < len) a += lds_f64(cb_s + 64u);
+                if (sl + 16 < len) a += lds_f64(cb_s + 128u);
+                for (int u = sl + 24; u < len; u += 8) a += lds_f64(sb_s + 8u * (unsigned)(off + u));
+                a += __shfl_xor_sync(FULL, a, 4);
+                a += __shfl_xor_sync(FULL, a, 2);
+                a += __shfl_xor_sync(FULL, a, 1);
+                const double got = __shfl_sync(FULL, a, (lane & 3) * 8);
+                if ((lane >> 2) == b) cval = got;
+            }
+            __syncwarp();                            // the buffer is rewritten by the next round
+        } else {
+            // a round too large for the buffer: direct 8-lane sums from global memory
+#pragma unroll
+            for (int b = 0; b < CPR / 4; ++b) {
+                const int src = 4 * b + sub;
+                const int64_t clo = __shfl_sync(FULL, mt.plo, src), chi = __shfl_sync(FULL, mt.phi, src);
+                double a = 0.0;
+                for (int64_t q = clo + sl; q < chi; q += 8) a = fma(__ldg(p_data + q), lds_f64(vs_s + 8u * (unsigned)__ldg(p_indices + q)), a);
+                a += __shfl_xor_sync(FULL, a, 4);
+                a += __shfl_xor_sync(FULL, a, 2);
+                a += __shfl_xor_sync(FULL, a, 1);
+                const double got = __shfl_sync(FULL, a, (lane & 3) * 8);
+                if ((lane >> 2) == b) cval = got;
+            }
+        }
+        if (mt.valid) epilogue(rd * CPR + lane, rd * CPR + lane, cval, mt.nrm, mt.bj);
+    };
+    const int64_t r0 = (int64_t)g.c * W + w;
+    if (r0 >= nround) return;
+    Buf A, B;
+    Meta m0 = load_meta(r0), m1 = load_meta(r0 + GW);
+    load_buf(m0, A);
+    for (int64_t rd = r0; rd < nround; rd += 2 * GW) {
+        Meta m2 = load_meta(rd + 2 * GW);
+        if (rd + GW < nround) load_buf(m1, B);
+        reduce_buf(rd, m0, A);
+        if (rd + GW >= nround) break;
+        Meta m3 = load_meta(rd + 3 * GW);
+        if (rd + 2 * GW < nround) load_buf(m2, A);
+        reduce_buf(rd + GW, m1, B);
+        m0 = m2;
+        m1 = m3;
+    }
+}
+
+// __noinline__: solve_body calls this from seven places; inlined, the kernel grew to
+// ~170 k instructions and the register pressure at the call sites pushed spills into
+// the CD chain's window loop (local-memory loads on the serial path).
 template <typename T>
-static __device__ void group_gemv(const Group& g, const SolveDev& P, const double* v, const int32_t* cols, int64_t m,
+static __device__ __forceinline__ void group_gemv_impl(const Group& g, const SolveDev& P, const double* v, const int32_t* cols, int64_t m,
                            int mode, double* out_c, float* out_t, double rho0, double gam, double radius,
                            double* vs, unsigned char* stg = nullptr, int64_t stg_bytes = 0,
                            int* tile_valid = nullptr) {
@@ -676,23 +822,37 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
     double bmax = -1.0;
     int64_t barg = INT64_MAX;
     const int64_t GW = (int64_t)g.G * W;
+    // P lives in global memory and every store below could alias it as far as the compiler
+    // knows, so each use would re-load the field (a dependent global load per column):
+    // the fields the epilogue needs are read once, here
+    const bool e_dome = P.rule == R_GAP_DOME && P.q != nullptr;
+    const double* __restrict__ e_q = P.q;
+    const double e_lam = P.lam;
+    const double e_R = e_dome ? P.sc->rule_R : 0.0, e_rd = e_dome ? P.sc->rule_rd : 0.0, e_a = e_dome ? P.sc->rule_a : 0.0;
+    uint8_t* const e_mark = P.mark;
     // per-column epilogue (lane 0); nrm/bj were loaded before the dot
     auto epilogue = [&](int64_t i, int64_t j, double cval, double nrm, double bj) {
         if (mode == G_MU) {
-            const double mu = (P.rule == R_GAP_DOME && P.q)
-                                  ? dome_mu(__ldg(P.q + j) / P.lam, cval, P.sc->rule_R, P.sc->rule_rd, P.sc->rule_a, nrm)
-                                  : fabs(cval) + radius * nrm;
-            P.mark[j] = (mu >= 1.0 - 1e-9) && nrm > 0.0;
+            const double mu = e_dome ? dome_mu(__ldg(e_q + j) / e_lam, cval, e_R, e_rd, e_a, nrm)
+                                     : fabs(cval) + radius * nrm;
+            e_mark[j] = (mu >= 1.0 - 1e-9) && nrm > 0.0;
         } else {
             if (out_c) out_c[i] = cval;
             argmax_merge(bmax, barg, fabs(cval), i);
             if (mode == G_CERT) {
-                const double tt = (bj != 0.0) ? -1.0 : cert_threshold(cval, nrm, P.lam, rho0, gam);
+                const double tt = (bj != 0.0) ? -1.0 : cert_threshold(cval, nrm, e_lam, rho0, gam);
                 out_t[i] = __double2float_rd(tt);
             }
         }
     };
-    if (P.sparse && P.csc_short) {
+    if (P.sparse && P.csc_short && stage && !cols && P.csc_flat &&
+        (int64_t)P.smem_total - (int64_t)(n + 2) * 8 >= (int64_t)W * 8 * 320) {
+        // consecutive columns (the full-p pass): flat coalesced loads, products parked in the
+        // shared memory left free beside the staged centre
+        const int64_t room = ((int64_t)P.smem_total - (int64_t)(n + 2) * 8) / ((int64_t)W * 8);
+        const int capw = (int)min((int64_t)512, room) & ~31;
+        group_gemv_csc_flat(g, P, vv, m, mode, vs + n + 2, capw, epilogue);
+    } else if (P.sparse && P.csc_short) {
         group_gemv_csc_short(g, P, vv, stage, cols, m, mode, epilogue);
     } else if (wide) {
         // vs is not staged in this mode: the ring takes the whole dynamic shared memory
@@ -718,7 +878,11 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
         // values are bit-identical to the direct path below.
         __shared__ unsigned long long s_gbar[kGStages];
         const T* X = (const T*)P.X;
-        const int64_t colb = P.ld * (int64_t)sizeof(T);
+        const int64_t ldx = P.ld;
+        const double* __restrict__ p_norms = P.norms;
+        const double* p_beta = P.beta;
+        const int use_hint = P.l2_hint, use_lds = P.lds_explicit;
+        const int64_t colb = ldx * (int64_t)sizeof(T);
         const int64_t sb = stg_bytes / kGStages / 16 * 16;
         const int C = (int)min((int64_t)(32 * W), sb / colb);      // columns per stage
         const int64_t per = (m + g.G - 1) / g.G;
@@ -740,12 +904,12 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             if (lane == 0) mbar_expect_tx_s(b, (unsigned)((i1 - i0) * colb));
             __syncwarp();
             if (!cols) {
-                if (lane == 0) tma_bulk_g2s_hint(dst, X + i0 * P.ld, (unsigned)((i1 - i0) * colb), b, pol_stream, P.l2_hint);
+                if (lane == 0) tma_bulk_g2s_hint(dst, X + i0 * ldx, (unsigned)((i1 - i0) * colb), b, pol_stream, use_hint);
             } else {
                 // one column per lane: the gathered indices load in parallel
                 for (int64_t i = i0 + lane; i < i1; i += 32)
-                    tma_bulk_g2s_hint(dst + (unsigned)((i - i0) * colb), X + (int64_t)cols[i] * P.ld, (unsigned)colb, b,
-                                      pol_stream, P.l2_hint);
+                    tma_bulk_g2s_hint(dst + (unsigned)((i - i0) * colb), X + (int64_t)cols[i] * ldx, (unsigned)colb, b,
+                                      pol_stream, use_hint);
             }
         };
         if (w == 0)
@@ -758,8 +922,8 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             jj = 0; nr = 0.0; bb = 0.0;
             if (k < nst && lane < per_w && i < min(hi, lo + (int64_t)(k + 1) * C)) {
                 jj = cols ? (int64_t)cols[i] : i;
-                nr = __ldg(P.norms + jj);
-                if (mode == G_CERT) bb = P.beta[jj];
+                nr = __ldg(p_norms + jj);
+                if (mode == G_CERT) bb = p_beta[jj];
             }
         };
         int64_t jn; double nn, bn;
@@ -780,8 +944,8 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             const T* base = reinterpret_cast<const T*>(stg + (size_t)s * sb);
             for (int l = 0; w + l * W < cn; ++l) {
                 const int cc = w + l * W;
-                const double cval = (stage && P.lds_explicit) ? ColDotSS<T>::run(stg0 + (unsigned)(s * sb) + (unsigned)(cc * colb), vs_s, n, lane)
-                                          : ColDotS<T>::run(base + (int64_t)cc * P.ld, vv, n, lane);
+                const double cval = (stage && use_lds) ? ColDotSS<T>::run(stg0 + (unsigned)(s * sb) + (unsigned)(cc * colb), vs_s, n, lane)
+                                          : ColDotS<T>::run(base + (int64_t)cc * ldx, vv, n, lane);
                 const int64_t j = __shfl_sync(0xffffffffu, jc, l);
                 const double nrm = __shfl_sync(0xffffffffu, nc, l);
                 const double bj = __shfl_sync(0xffffffffu, bc, l);
@@ -825,6 +989,14 @@ static __device__ void group_gemv(const Group& g, const SolveDev& P, const doubl
             P.cta_idx[g.c] = barg;
         }
     }
+}
+
+template <typename T>
+static __device__ __noinline__ void group_gemv(const Group& g, const SolveDev& P, const double* v, const int32_t* cols, int64_t m,
+                           int mode, double* out_c, float* out_t, double rho0, double gam, double radius,
+                           double* vs, unsigned char* stg = nullptr, int64_t stg_bytes = 0,
+                           int* tile_valid = nullptr) {
+    group_gemv_impl<T>(g, P, v, cols, m, mode, out_c, out_t, rho0, gam, radius, vs, stg, stg_bytes, tile_valid);
 }
 
 // max over the per-CTA partials (every caller thread gets the same answer)
@@ -2943,7 +3115,7 @@ __global__ void __launch_bounds__(256, 1) k_screen_full(const SolveDev* __restri
     extern __shared__ __align__(16) unsigned char smem[];
     const SolveDev& P = probs[0];
     Group g{(int)gridDim.x, (int)blockIdx.x, nullptr};
-    group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, 0.0, radius,
+    group_gemv_impl<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, 0.0, radius,
                   reinterpret_cast<double*>(smem + (P.sparse ? 0 : P.cd_bytes)), smem, P.sparse ? 0 : P.cd_bytes,
                   nullptr);
 }
