@@ -182,6 +182,13 @@ static __device__ __forceinline__ void spin_guard(unsigned long long t0, int whe
     if (gtimer() - t0 > 20000000000ull) spin_fail(where, a, b, c, d);
 }
 
+// the same, consulted only every 256th poll: %globaltimer is slow to read, and a poll loop
+// that reads it every time notices the awaited event late
+static __device__ __forceinline__ void spin_guard_sparse(unsigned& it, unsigned long long t0, int where = 0, int a = 0,
+                                                        int b = 0, int c = 0, int d = 0) {
+    if ((++it & 255u) == 0u) spin_guard(t0, where, a, b, c, d);
+}
+
 static __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 static __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -473,7 +480,8 @@ static __device__ __noinline__ void group_gemv_wide(const Group& g, const SolveD
             const unsigned b = bar0 + 8u * s, par = (unsigned)((k / NS) & 1);
             if (!mbar_test_s(b, par)) {
                 const unsigned long long t0 = gtimer();
-                while (!mbar_test_s(b, par)) spin_guard(t0, 6, k, nst, (int)g.c, 0);
+                unsigned it = 0;
+                while (!mbar_test_s(b, par)) spin_guard_sparse(it, t0, 6, k, nst, (int)g.c, 0);
             }
         }
         const unsigned base_s = stg0 + (unsigned)(s * colb);
@@ -808,7 +816,8 @@ static __device__ __forceinline__ void group_gemv_impl(const Group& g, const Sol
             __syncthreads();
             if (!mbar_test_s(vb, 0)) {
                 const unsigned long long t0 = gtimer();
-                while (!mbar_test_s(vb, 0)) spin_guard(t0, 7, n, 0, 0, 0);
+                unsigned it = 0;
+                while (!mbar_test_s(vb, 0)) spin_guard_sparse(it, t0, 7, n, 0, 0, 0);
             }
             __syncthreads();
             if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(vb) : "memory");
@@ -936,7 +945,8 @@ static __device__ __forceinline__ void group_gemv_impl(const Group& g, const Sol
                 const unsigned b = bar0 + 8u * s, par = (unsigned)((k / kGStages) & 1);
                 if (!mbar_test_s(b, par)) {
                     const unsigned long long t0 = gtimer();
-                    while (!mbar_test_s(b, par)) spin_guard(t0, 5, k, nst, (int)g.c, 0);
+                    unsigned it = 0;
+                    while (!mbar_test_s(b, par)) spin_guard_sparse(it, t0, 5, k, nst, (int)g.c, 0);
                 }
             }
             const int64_t i0 = lo + (int64_t)k * C;
@@ -1940,7 +1950,8 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 const unsigned par = (unsigned)((k >> kshift) & 1);
                 if (!mbar_test_s(bar_s + 8u * s, par)) {
                     const unsigned long long t0 = gtimer();
-                    while (!mbar_test_s(bar_s + 8u * s, par)) spin_guard(t0, 4, k, gen, last, 0);
+                    unsigned it = 0;
+                    while (!mbar_test_s(bar_s + 8u * s, par)) spin_guard_sparse(it, t0, 4, k, gen, last, 0);
                 }
                 const SlotHdr* h0 = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
                 pos = h0->pos; hg = h0->gen; j = h0->j; tc = h0->tcert; dp = h0->dp;

@@ -284,3 +284,34 @@ def test_fused_screen_pass_matches_oracle(kind):
         diff = np.setxor1d(a, b.active_set)
         assert np.all(near[diff]), (kind, r, diff[:5])
         assert a.size > 0 or b.active_set.size == 0
+
+
+def test_design_constructors_blockwise_and_device():
+    """Block-wise upload (designs larger than a host array), the device-buffer
+    constructor (columns received over NCCL) and the device column gather give
+    the same design as the host-array constructor."""
+    torch = pytest.importorskip("torch")
+    for dtype in (np.float64, np.float32):
+        X, rng = _dense(31, 130, 700, dtype)
+        v = rng.standard_normal(130)
+        D = gs.DesignMatrix(X)
+        blocks = ((j0, X[:, j0:j0 + 256]) for j0 in range(0, 700, 256))
+        Db = gs.DesignMatrix.from_blocks(130, 700, dtype, blocks)
+        assert np.array_equal(Db.col_norms_sq, D.col_norms_sq)
+        assert np.array_equal(Db.transpose_dot(v), D.transpose_dot(v))
+        assert Db.max_abs_correlation(v) == D.max_abs_correlation(v)
+        idx = np.array([699, 0, 17, 17, 345], dtype=np.int64)
+        assert np.array_equal(D.columns_to_host(idx), X[:, idx])
+        # device buffer -> design: the gathered columns as a (k, n) CUDA tensor
+        tdt = torch.float32 if dtype == np.float32 else torch.float64
+        buf = torch.empty((idx.size, 130), dtype=tdt, device="cuda")
+        D.gather_columns_to_device(idx, buf.data_ptr(), 130)
+        torch.cuda.synchronize()
+        Dd = gs.DesignMatrix.from_device(buf.data_ptr(), 130, idx.size, 130, dtype)
+        ref = gs.DesignMatrix(np.asfortranarray(X[:, idx]))
+        assert np.array_equal(Dd.col_norms_sq, ref.col_norms_sq)
+        assert np.array_equal(Dd.transpose_dot(v), ref.transpose_dot(v))
+        with pytest.raises(ValueError):
+            Dd.toarray()
+    with pytest.raises(IndexError):
+        D.columns_to_host(np.array([700], dtype=np.int64))
