@@ -94,12 +94,8 @@ __host__ __device__ inline size_t blk_smem_bytes(int64_t ld, int es) {
 static __device__ __forceinline__ void blk_wait(unsigned bar, int use, int where) {
     const unsigned par = (unsigned)(use & 1);
     if (!mbar_test_s(bar, par)) {
-        // the watchdog reads %globaltimer (slow): only every 256th poll, so that the
-        // completion is noticed within a few cycles of the phase flip
         const unsigned long long t0 = gtimer();
-        unsigned it = 0;
-        while (!mbar_test_s(bar, par))
-            if ((++it & 255u) == 0u) spin_guard(t0, where, use, 0, 0, 0);
+        while (!mbar_test_s(bar, par)) spin_guard(t0, where, use, 0, 0, 0);
     }
 }
 
@@ -171,7 +167,6 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
             bool stop = false;
             {
                 const unsigned long long t0 = gtimer();
-                unsigned it = 0;
                 for (;;) {
                     if (ld_acq_s(done_s)) { stop = true; break; }
                     const int rg = ld_acq_s(reqg_s);
@@ -184,7 +179,7 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
                         emitted_last = false;
                     }
                     if (!emitted_last && ld_acq_s(cons_s) >= q - 1) break;
-                    if ((++it & 255u) == 0u) spin_guard(t0, 13, q, gen, cur, 0);
+                    spin_guard(t0, 13, q, gen, cur, 0);
                 }
             }
             if (stop) break;
@@ -415,12 +410,7 @@ static __device__ __noinline__ void cd_epoch_blk(const SolveDev& P, int64_t m64,
                 if (b < ncommit && use_t) D = Dv[b];
                 if (lane == b) { dmine = d; nbmine = nbv[b]; }
             }
-            if (nzc) {
-                // mean drift increment of the committed nonzero members (1/nzc by selects: no DDIV)
-                const double rn = nzc == 1 ? 1.0 : nzc == 2 ? 0.5 : nzc == 3 ? (1.0 / 3.0) : nzc == 4 ? 0.25
-                                  : nzc == 5 ? 0.2 : nzc == 6 ? (1.0 / 6.0) : (1.0 / 7.0);
-                gstep = 0.5 * gstep + 0.5 * (ssum * rn);
-            }
+            if (nzc) gstep = 0.5 * gstep + 0.5 * (ssum / (double)nzc);
             if (w == 0 && lane < ncommit && dmine != 0.0) {
                 // lane b commits member b (values of its own chain copy)
                 const int j = dsc->j[lane], pos = dsc->pos[lane];

@@ -182,13 +182,6 @@ static __device__ __forceinline__ void spin_guard(unsigned long long t0, int whe
     if (gtimer() - t0 > 20000000000ull) spin_fail(where, a, b, c, d);
 }
 
-// the same, consulted only every 256th poll: %globaltimer is slow to read, and a poll loop
-// that reads it every time notices the awaited event late
-static __device__ __forceinline__ void spin_guard_sparse(unsigned& it, unsigned long long t0, int where = 0, int a = 0,
-                                                        int b = 0, int c = 0, int d = 0) {
-    if ((++it & 255u) == 0u) spin_guard(t0, where, a, b, c, d);
-}
-
 static __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 static __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -480,8 +473,7 @@ static __device__ __noinline__ void group_gemv_wide(const Group& g, const SolveD
             const unsigned b = bar0 + 8u * s, par = (unsigned)((k / NS) & 1);
             if (!mbar_test_s(b, par)) {
                 const unsigned long long t0 = gtimer();
-                unsigned it = 0;
-                while (!mbar_test_s(b, par)) spin_guard_sparse(it, t0, 6, k, nst, (int)g.c, 0);
+                while (!mbar_test_s(b, par)) spin_guard(t0, 6, k, nst, (int)g.c, 0);
             }
         }
         const unsigned base_s = stg0 + (unsigned)(s * colb);
@@ -816,8 +808,7 @@ static __device__ __forceinline__ void group_gemv_impl(const Group& g, const Sol
             __syncthreads();
             if (!mbar_test_s(vb, 0)) {
                 const unsigned long long t0 = gtimer();
-                unsigned it = 0;
-                while (!mbar_test_s(vb, 0)) spin_guard_sparse(it, t0, 7, n, 0, 0, 0);
+                while (!mbar_test_s(vb, 0)) spin_guard(t0, 7, n, 0, 0, 0);
             }
             __syncthreads();
             if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(vb) : "memory");
@@ -945,8 +936,7 @@ static __device__ __forceinline__ void group_gemv_impl(const Group& g, const Sol
                 const unsigned b = bar0 + 8u * s, par = (unsigned)((k / kGStages) & 1);
                 if (!mbar_test_s(b, par)) {
                     const unsigned long long t0 = gtimer();
-                    unsigned it = 0;
-                    while (!mbar_test_s(b, par)) spin_guard_sparse(it, t0, 5, k, nst, (int)g.c, 0);
+                    while (!mbar_test_s(b, par)) spin_guard(t0, 5, k, nst, (int)g.c, 0);
                 }
             }
             const int64_t i0 = lo + (int64_t)k * C;
@@ -1950,8 +1940,7 @@ static __device__ __noinline__ void cd_epoch_dense(const SolveDev& P, int64_t m6
                 const unsigned par = (unsigned)((k >> kshift) & 1);
                 if (!mbar_test_s(bar_s + 8u * s, par)) {
                     const unsigned long long t0 = gtimer();
-                    unsigned it = 0;
-                    while (!mbar_test_s(bar_s + 8u * s, par)) spin_guard_sparse(it, t0, 4, k, gen, last, 0);
+                    while (!mbar_test_s(bar_s + 8u * s, par)) spin_guard(t0, 4, k, gen, last, 0);
                 }
                 const SlotHdr* h0 = reinterpret_cast<const SlotHdr*>(ring + (size_t)s * sbytes);
                 pos = h0->pos; hg = h0->gen; j = h0->j; tc = h0->tcert; dp = h0->dp;
@@ -2458,79 +2447,112 @@ static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t 
             __syncthreads();
         }
         const int tb = s_tb, tend = s_tend;
-        // ---------------- admission (warp 0, one ballot per 32 positions) ----------------
+        // ---------------- admission (warp 0) ----------------
+        // Pass 1 scans the staged thresholds only (shared memory): up to kSpMW uncertified
+        // positions, lane k ends up with candidate k.  Pass 2 loads the candidates' column
+        // pointers and constants in ONE parallel round (the round-1 version loaded them
+        // inside the scan loop, a dependent global round trip per 32 positions).
         if (w == 0) {
             const double D = s_D;
             const double dp = use_t ? __dadd_ru(D, __dmul_ru(2.0 * kSpMW, gstep)) : 0.0;
-            int nmem = 0, b = -1, solo = 0;
-            for (int base = a; b < 0; base += 32) {
-                if (base >= tend) { b = tend; break; }
+            int nmem = 0, b = tend, solo = 0;
+            for (int base = a; base < tend && nmem < kSpMW; base += 32) {
                 const int q = base + lane;
                 const bool unc = q < tend && (!use_t || !(dp < (double)ts[q - tb]));
                 const unsigned mask = __ballot_sync(FULL, unc);
-                if (!mask) continue;
-                int cj = 0, cnz = 0;
-                int64_t clo = 0;
-                if (unc) {
-                    cj = As[q - tb];
-                    clo = __ldg(P.indptr + cj);
-                    cnz = (int)(__ldg(P.indptr + cj + 1) - clo);
+                const int cntm = __popc(mask), room = kSpMW - nmem, take = min(cntm, room);
+                const int rank = __popc(mask & ((1u << lane) - 1u));
+                if (unc && rank < take) s_flag[nmem + rank] = q;          // candidate list (positions)
+                nmem += take;
+                if (take < cntm) {
+                    // the wave ends before the first candidate that did not fit
+                    const unsigned nxt = __ballot_sync(FULL, unc && rank == take);
+                    b = base + __ffs((int)nxt) - 1;
+                    break;
                 }
-                unsigned take = mask;
-                const unsigned longm = __ballot_sync(FULL, unc && cnz > 32);
-                if (longm) {
-                    const int fl = __ffs(longm) - 1;
-                    const unsigned before = mask & ((1u << fl) - 1u);
-                    if (nmem == 0 && before == 0u) { take = 1u << fl; solo = 1; b = base + fl + 1; }
-                    else { take = before; b = base + fl; }
-                }
-                const int room = kSpMW - nmem;
-                if (__popc(take) >= room) {
-                    const int lb = (int)__fns(take, 0, room);
-                    take &= (lb == 31) ? FULL : ((2u << lb) - 1u);
-                    b = base + lb + 1;
-                }
-                if ((take >> lane) & 1u) {
-                    const int k = nmem + __popc(take & ((1u << lane) - 1u));
-                    SpMember& M = mem[k];
-                    M.pos = q; M.j = cj; M.nnz = cnz;
-                    M.ns = __ldg(P.nsq + cj); M.nr = __ldg(P.norms + cj); M.bj = P.beta[cj];
-                    s_lo[k] = clo;
-                }
-                nmem += __popc(take);
+                if (nmem == kSpMW) { b = min(base + 32, tend); break; }
+            }
+            __syncwarp();
+            int q = 0, cj = 0, cnz = 0;
+            int64_t clo = 0;
+            double c_ns = 0.0, c_nr = 0.0, c_bj = 0.0;
+            if (lane < nmem) {
+                q = s_flag[lane];
+                cj = As[q - tb];
+                clo = __ldg(P.indptr + cj);
+                cnz = (int)(__ldg(P.indptr + cj + 1) - clo);
+                c_ns = __ldg(P.nsq + cj); c_nr = __ldg(P.norms + cj); c_bj = P.beta[cj];
+            }
+            // a column with more than 32 nonzeros ends the wave before it, or runs alone
+            const unsigned longm = __ballot_sync(FULL, lane < nmem && cnz > 32);
+            if (longm) {
+                const int fl = __ffs((int)longm) - 1;
+                if (fl == 0) { nmem = 1; solo = 1; b = __shfl_sync(FULL, q, 0) + 1; }
+                else { nmem = fl; b = __shfl_sync(FULL, q, fl); }
+            }
+            if (lane < nmem) {
+                SpMember& M = mem[lane];
+                M.pos = q; M.j = cj; M.nnz = cnz;
+                M.ns = c_ns; M.nr = c_nr; M.bj = c_bj;
+                s_lo[lane] = clo;
             }
             if (lane == 0) { s_b = b; s_nmem = nmem; s_solo = solo; }
         }
         __syncthreads();
         const int nmem = s_nmem;
         // ---------------- g and d of every member from the wave-start rho ----------------
-        double oldv[(kSpMW + 7) / 8];
+        // the (up to four) members of this warp are loaded together: one global round trip
+        // for their row indices and values instead of one per member
+        constexpr int kIt = (kSpMW + 7) / 8;
+        double oldv[kIt];
+        if (!s_solo) {
+            int rr_[kIt];
+            double xx_[kIt];
 #pragma unroll
-        for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
-            oldv[it] = 0.0;
-            const int k = w + it * NW;
-            if (k >= nmem) continue;
-            SpMember& M = mem[k];
-            double g, x = 0.0, o = 0.0;
-            const int64_t lo = s_lo[k];
-            if (!s_solo) {
-                int r = -1;
-                if (lane < M.nnz) { r = __ldg(P.indices + lo + lane); x = __ldg(P.data + lo + lane); o = srho[r]; }
-                if (lane < 32) { M.idx[lane] = r; M.val[lane] = x; }
-                g = warp_sum(fma(x, o, 0.0));
-            } else {
-                const int64_t hi = lo + M.nnz;
+            for (int it = 0; it < kIt; ++it) {
+                const int k = w + it * NW;
+                rr_[it] = -1; xx_[it] = 0.0;
+                if (k < nmem && lane < mem[k].nnz) {
+                    const int64_t lo = s_lo[k];
+                    rr_[it] = __ldg(P.indices + lo + lane);
+                    xx_[it] = __ldg(P.data + lo + lane);
+                }
+            }
+#pragma unroll
+            for (int it = 0; it < kIt; ++it) {
+                oldv[it] = 0.0;
+                const int k = w + it * NW;
+                if (k >= nmem) continue;
+                SpMember& M = mem[k];
+                const int r = rr_[it];
+                const double x = xx_[it];
+                const double o = r >= 0 ? srho[r] : 0.0;
+                M.idx[lane] = r; M.val[lane] = x;
+                const double g = warp_sum(fma(x, o, 0.0));
+                const double z = M.bj + g / M.ns;
+                const double u = lam / M.ns;
+                const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+                const double d = nb - M.bj;
+                oldv[it] = o;
+                __syncwarp();
+                if (lane == 0) { M.d = d; M.nb = nb; M.step = d != 0.0 ? __dmul_ru(fabs(d), M.nr) : 0.0; }
+            }
+        } else {
+#pragma unroll
+            for (int it = 0; it < kIt; ++it) oldv[it] = 0.0;
+            if (w == 0 && nmem > 0) {
+                SpMember& M = mem[0];
+                const int64_t lo = s_lo[0], hi = lo + M.nnz;
                 double acc = 0.0;
                 for (int64_t q = lo + lane; q < hi; q += 32) acc = fma(__ldg(P.data + q), srho[__ldg(P.indices + q)], acc);
-                g = warp_sum(acc);
+                const double g = warp_sum(acc);
+                const double z = M.bj + g / M.ns;
+                const double u = lam / M.ns;
+                const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
+                const double d = nb - M.bj;
+                __syncwarp();
+                if (lane == 0) { M.d = d; M.nb = nb; M.step = d != 0.0 ? __dmul_ru(fabs(d), M.nr) : 0.0; }
             }
-            const double z = M.bj + g / M.ns;
-            const double u = lam / M.ns;
-            const double nb = z > u ? z - u : (z < -u ? z + u : 0.0);
-            const double d = nb - M.bj;
-            oldv[it] = o;
-            __syncwarp();
-            if (lane == 0) { M.d = d; M.nb = nb; M.step = d != 0.0 ? __dmul_ru(fabs(d), M.nr) : 0.0; }
         }
         __syncthreads();
         // ---------------- conflicts with earlier nonzero members (row map) ----------------
@@ -2541,12 +2563,17 @@ static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t 
                 if (k < nmem && mem[k].d != 0.0 && lane < mem[k].nnz) atomicMin(first + mem[k].idx[lane], k);
             }
             __syncthreads();
+            int own[(kSpMW + 7) / 8];
+#pragma unroll
+            for (int it = 0; it < (kSpMW + 7) / 8; ++it) {        // the four row-map reads in one round trip
+                const int k = w + it * NW;
+                own[it] = (k < nmem && lane < mem[k].nnz) ? __ldcg(first + mem[k].idx[lane]) : 0x7fffffff;
+            }
 #pragma unroll
             for (int it = 0; it < (kSpMW + 7) / 8; ++it) {
                 const int k = w + it * NW;
                 if (k >= nmem) continue;
-                const bool hit = lane < mem[k].nnz && __ldcg(first + mem[k].idx[lane]) < k;
-                const unsigned hb = __ballot_sync(FULL, hit);
+                const unsigned hb = __ballot_sync(FULL, own[it] < k);
                 if (lane == 0) s_flag[k] = hb != 0u;
             }
             __syncthreads();
