@@ -192,11 +192,7 @@ extern "C" int gs_matrix_csc(const double* data, const int32_t* indices, const i
     int rc;
     if ((rc = [&]() -> int {
             CK(cudaStreamCreateWithFlags(&M->st, cudaStreamNonBlocking));
-            // + 8 entries: the sequential CD chain copies 16-byte aligned spans that may reach
-            // up to 3 entries past the last column (never used, but they must be addressable)
-            TRY(dalloc(&M->data, nnz + 8)); TRY(dalloc(&M->indices, nnz + 8)); TRY(dalloc(&M->indptr, p + 1));
-            CK(cudaMemsetAsync(M->data + nnz, 0, 8 * sizeof(double), M->st));
-            CK(cudaMemsetAsync(M->indices + nnz, 0, 8 * sizeof(int32_t), M->st));
+            TRY(dalloc(&M->data, nnz)); TRY(dalloc(&M->indices, nnz)); TRY(dalloc(&M->indptr, p + 1));
             CK(cudaMemcpyAsync(M->data, data, nnz * 8, cudaMemcpyHostToDevice, M->st));
             CK(cudaMemcpyAsync(M->indices, indices, nnz * 4, cudaMemcpyHostToDevice, M->st));
             CK(cudaMemcpyAsync(M->indptr, indptr, (p + 1) * 8, cudaMemcpyHostToDevice, M->st));
@@ -693,18 +689,10 @@ static bool csc_short_for(const gs_matrix* M) {
     return M->p > 0 && M->nnz <= 24 * M->p;
 }
 
-// CSC CD: the sequential chain with a producer warp when every column has at most 32 nonzeros
-static bool csc_seq_for(const gs_matrix* M) {
-    if (!M->sparse) return false;
-    const char* e = getenv("GS_CSC_SEQ");
-    if (e && atoi(e) == 0) return false;
-    return M->max_col_nnz <= kSqMaxNnz;
-}
-
 static size_t solve_smem(const gs_matrix* M) {
     const int64_t n = M->n;
     const size_t vs = (n <= vs_cap_for(M) && !gemv_wide_for(M)) ? (size_t)(n + 2) * 8 : 0;
-    if (M->sparse) return std::max(vs, std::max(cd_csc_smem_bytes(n), csc_seq_for(M) ? cd_csc_seq_smem_bytes(n) : (size_t)0));
+    if (M->sparse) return std::max(vs, cd_csc_smem_bytes(n));
     size_t b = cd_bytes_for(M) + vs;     // dense: CD tile + column ring stay resident beside the GEMV staging
     if (gemv_wide_for(M)) {
         // the column ring of the wide GEMV takes all of it: as many whole columns as fit (up to 8)
@@ -722,7 +710,6 @@ static void set_plan(const gs_matrix* M, SolveDev& d) {
     d.cd_bytes = (int)cd_bytes_for(M);
     d.gemv_wide = gemv_wide_for(M) ? 1 : 0;
     d.csc_short = csc_short_for(M) ? 1 : 0;
-    d.csc_seq = csc_seq_for(M) ? 1 : 0;
     d.smem_total = (int)solve_smem(M);
     const char* efl = getenv("GS_CSC_FLAT");
     d.csc_flat = efl ? atoi(efl) : 1;

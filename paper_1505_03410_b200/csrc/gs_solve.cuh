@@ -127,7 +127,6 @@ struct SolveDev {
     int csc_short;       // CSC GEMV: 8 lanes per column (short columns), 32 columns per warp round
     int smem_total;      // dynamic shared memory of the launch (bytes)
     int cd_chunk_pos;    // sparse CD: positions per re-anchored chunk of an epoch (0: whole epoch)
-    int csc_seq;         // CSC CD: sequential chain with a producer warp (columns of <= 32 nonzeros)
     int csc_flat;        // CSC full-p pass: flat coalesced loads + products in shared memory
     int l2_hint;         // TMA copies carry L2 eviction-priority hints (GEMV evict_first, CD columns evict_last)
     int lds_explicit;    // staged GEMV reads shared memory through ld.shared on 32-bit addresses
@@ -2719,7 +2718,6 @@ static __device__ __noinline__ void cd_epoch_csc_par(const SolveDev& P, int64_t 
 // ---------------------------------------------------------------------------
 }  // namespace gs
 #include "gs_cd_blk.cuh"
-#include "gs_cd_csc_seq.cuh"
 namespace gs {
 
 // dense CD epoch: blocked chain (cd_gram == 2, R <= 5) or the ring consumers
@@ -3031,9 +3029,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
                 if (g.c == 0) {
                     const unsigned long long td0 = gtimer();
                     if (threadIdx.x == 0) ctl->t_refresh += td0 - tr0;
-                    if (P.csc_seq) cd_epoch_csc_seq(P, c1, smem, c0);
-                    else if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, c1, smem, c0);
-                    else cd_epoch_csc(P, c1, smem, c0);
+                    if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, c1, smem, c0); else cd_epoch_csc(P, c1, smem, c0);
                     if (threadIdx.x == 0) ctl->t_cd += gtimer() - td0;
                     unc += ctl->epoch_unc; nz += ctl->epoch_nz;
                 }
@@ -3058,11 +3054,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
         }
         if (g.c == 0) {
             const unsigned long long td0 = gtimer();
-            if (P.sparse) {
-                if (P.csc_seq) cd_epoch_csc_seq(P, m, smem);
-                else if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, m, smem);
-                else cd_epoch_csc(P, m, smem);
-            }
+            if (P.sparse) { if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, m, smem); else cd_epoch_csc(P, m, smem); }
             else cd_epoch_dense_any<T, R>(P, m, smem, &s_tile_valid);
             if (threadIdx.x == 0) {
                 ctl->t_cd += gtimer() - td0;
