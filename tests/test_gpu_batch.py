@@ -61,3 +61,31 @@ def test_batch_more_problems_than_sms_schedule_independent():
         assert np.array_equal(one["passes"][0], res["passes"][b]), b
         assert np.array_equal(one["gaps"][0], res["gaps"][b]), b
         assert np.array_equal(one["n_active"][0], res["n_active"][b]), b
+
+
+def test_cfg4_full_width_per_problem_eps():
+    """configs[4] at its stated width (the shared 1000 x 50000 design, n = 500
+    bootstrap rows), B = 16 problems each at its own eps_b = 1e-8 ||y_b||^2,
+    on the first grid points of the 50-lambda grid: two of the problems are
+    checked against the oracle's run_path on the same resampled rows."""
+    X0, y0, _ = synth.cfg4_shared()
+    B, T, K = 16, 50, 14
+    rows = np.stack([synth.cfg4_rows(b) for b in range(B)]).astype(np.int32)
+    D0 = gs.DesignMatrix(X0)
+    bs = gs.BatchPathSolver(D0, y0, rows)
+    grids = np.stack([gs.lambda_grid(bs.lambda_max[b], T, 2.0)[:K] for b in range(B)])
+    eps = np.array([1e-8 * float(y0[rows[b]] @ y0[rows[b]]) for b in range(B)])
+    res = bs.run_paths(grids, gs.SolverConfig(epsilon=1.0, max_passes=100_000), want_betas=True, epsilons=eps)
+    assert np.all(res["converged"])
+    for b in (3, 12):
+        Xb = np.asfortranarray(X0[rows[b]])
+        yb = y0[rows[b]]
+        ref = O.run_path(O.DesignMatrix(Xb), yb, grids[b], O.SolverConfig(epsilon=float(eps[b]), max_passes=100_000))
+        yy = float(yb @ yb)
+        for t in range(K):
+            st = ref.states[t]
+            assert res["passes"][b, t] == st.passes_done, (b, t)
+            assert res["n_active"][b, t] == st.active.size, (b, t)
+            assert np.array_equal(np.flatnonzero(res["betas"][b, t]), np.flatnonzero(st.beta)), (b, t)
+            assert beta_close(res["betas"][b, t], st.beta), (b, t)
+            assert gap_close(res["gaps"][b, t], st.cert.gap, yy), (b, t)
