@@ -2734,16 +2734,21 @@ template <typename T, int R>
 static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned char* smem) {
     __shared__ int sh[32];
     __shared__ double red[32];
+    // CSC designs always launch the R = 1 instantiation (gs_api.cu: launch_solve): the
+    // long-column instantiation compiles the sparse branches out, which leaves the direct
+    // CD chain (96 registers of rho) a leaner caller
+    constexpr bool kMaySparse = R < 48;
+    const bool sparse_ = kMaySparse && P.sparse;
     DevScalars* sc = P.sc;
     SolveCtl* ctl = P.ctl;
     // dense: [CD tile | vs]; sparse: the CD uses [t tile | rho] and vs aliases it
-    double* vs = reinterpret_cast<double*>(smem + (P.sparse ? 0 : P.cd_bytes));
+    double* vs = reinterpret_cast<double*>(smem + (sparse_ ? 0 : P.cd_bytes));
     __shared__ int s_tile_valid;
     if (threadIdx.x == 0) s_tile_valid = 0;
     __syncthreads();
     const bool gap_rule = P.rule == R_GAP_SPHERE;
     const bool screening = P.rule != R_NONE;
-    const double gam = gamma_n(P.sparse ? (int64_t)P.n : (int64_t)P.n);
+    const double gam = gamma_n(sparse_ ? (int64_t)P.n : (int64_t)P.n);
 
     if (ctl->done) return;
 
@@ -2795,7 +2800,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
             group_sync(g);
             if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
             const unsigned long long ts0 = gtimer();
-            group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, gam, sc->radius, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
+            group_gemv<T>(g, P, P.theta, nullptr, P.p, G_MU, nullptr, nullptr, 0.0, gam, sc->radius, vs, smem, sparse_ ? 0 : P.cd_bytes, &s_tile_valid);
             group_sync(g);
             if (g.c == 0 && threadIdx.x == 0) { ctl->t_screen += gtimer() - ts0; ctl->n_screen++; }
         } else if (P.init_mode == 0) {
@@ -2821,7 +2826,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
             if (!P.mark[j]) P.beta[j] = 0.0;
             P.mark[j] = 0;
             const double ns = __ldg(P.nsq + j);
-            if (!P.sparse) {
+            if (!sparse_) {
                 ColInfo ci;
                 ci.ns = ns;
                 ci.inv = __ldg(P.inv_nsq + j);
@@ -2863,7 +2868,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
             group_resync<T>(g, P, m, sh);
             if (m == 0) {
                 // everything screened: unrestricted dual point (solver.py:190-203)
-                group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
+                group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, sparse_ ? 0 : P.cd_bytes, &s_tile_valid);
                 group_sync(g);
                 if (g.c == 0) {
                     double corr; int64_t ci;
@@ -2885,7 +2890,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
                 if (sc->status != ST_OK) { if (g.c == 0 && threadIdx.x == 0) ctl->done = 1; return; }
             } else {
                 // restricted |X_A^T rho|_inf with the dots kept for mu and the anchor
-                group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, P.c, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
+                group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, P.c, nullptr, 0.0, gam, 0.0, vs, smem, sparse_ ? 0 : P.cd_bytes, &s_tile_valid);
                 group_sync(g);
                 if (g.c == 0) {
                     double corr; int64_t ci;
@@ -2925,7 +2930,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
                     // drop axpys rho += beta_j x_j, ascending j (numpy order per element)
                     const int64_t nd = sc->n_drop;
                     if (nd > 0) {
-                        if (P.sparse) {
+                        if (sparse_) {
                             if (g.c == 0) {
                                 for (int64_t q0 = 0; q0 < nd; ++q0) {
                                     const int32_t j = P.Dl[q0];
@@ -3015,7 +3020,7 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
         // a few hundred updates have accumulated; with the drift restarted per chunk the
         // uncertified visits fall to about the support (exact skips only, so the
         // arithmetic is unchanged).  One pass over X_A per epoch in total.
-        const int nch = (P.sparse && P.certify && P.cd_chunk_pos > 0 && m > 0)
+        const int nch = (sparse_ && P.certify && P.cd_chunk_pos > 0 && m > 0)
                             ? (int)imin64(256, imax64(1, (m + P.cd_chunk_pos - 1) / P.cd_chunk_pos)) : 1;
         if (nch > 1) {
             int64_t unc = 0, nz = 0;
@@ -3047,14 +3052,14 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
         if (P.certify && ctl->need_refresh && m > 0) {
             const unsigned long long tr0 = gtimer();
             const double anchor = sc->rho_norm_ub;
-            group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
+            group_gemv<T>(g, P, P.rho, P.A, m, G_CERT, P.c, P.t, anchor, gam, 0.0, vs, smem, sparse_ ? 0 : P.cd_bytes, &s_tile_valid);
             if (g.c == 0 && threadIdx.x == 0) { ctl->anchor_norm = anchor; ctl->cd_delta = 0.0; ctl->n_refresh++; s_tile_valid = 0; }
             group_sync(g);
             if (g.c == 0 && threadIdx.x == 0) ctl->t_refresh += gtimer() - tr0;
         }
         if (g.c == 0) {
             const unsigned long long td0 = gtimer();
-            if (P.sparse) { if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, m, smem); else cd_epoch_csc(P, m, smem); }
+            if (sparse_) { if (P.csc_par && P.rowmark) cd_epoch_csc_par(P, m, smem); else cd_epoch_csc(P, m, smem); }
             else cd_epoch_dense_any<T, R>(P, m, smem, &s_tile_valid);
             if (threadIdx.x == 0) {
                 ctl->t_cd += gtimer() - td0;
@@ -3069,8 +3074,8 @@ static __device__ void solve_body(const SolveDev& P, const Group& g, unsigned ch
     if (!converged) {
         const int64_t m = sc->m;
         group_resync<T>(g, P, m, sh);
-        if (m > 0) group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
-        else group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, P.sparse ? 0 : P.cd_bytes, &s_tile_valid);
+        if (m > 0) group_gemv<T>(g, P, P.rho, P.A, m, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, sparse_ ? 0 : P.cd_bytes, &s_tile_valid);
+        else group_gemv<T>(g, P, P.rho, nullptr, P.p, G_DUAL, nullptr, nullptr, 0.0, gam, 0.0, vs, smem, sparse_ ? 0 : P.cd_bytes, &s_tile_valid);
         group_sync(g);
         if (g.c == 0) {
             double corr; int64_t ci;
